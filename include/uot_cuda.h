@@ -1,0 +1,159 @@
+/*
+ * uot_cuda.h — C ABI of the B200-native fused Sinkhorn-UOT solver.
+ *
+ * This is the drop-in boundary for the reference's solver API
+ * (/root/reference/proj/core/include/uot, "namespace uot"). The reference has no
+ * FFI of its own: its boundary is header-only C++ templates. Each entry point
+ * below states the reference interface it replaces. A C++ facade with the
+ * reference's exact types and exception classes sits on top
+ * (include/uot/cuda.hpp); Python binds it with ctypes
+ * (paper_2412_11079_b200/uot.py). See INTEGRATION.md.
+ *
+ * Conventions: plain pointers and sizes only; host buffers unless a name says
+ * _device; every call returns a status code and never throws across the ABI.
+ * The problem stays resident in HBM between calls ("session"): the reference's
+ * per-iteration API mutates a host Matrix<T>& in place (fused.hpp:164-191),
+ * which at 4 GiB per iteration would be PCIe-bound, so the host matrix is only
+ * touched by uot_set_problem / uot_get_plan.
+ */
+#ifndef UOT_CUDA_H
+#define UOT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: the reference exception hierarchy (include/uot/error.hpp:9-37). */
+#define UOT_OK 0
+#define UOT_INVALID_PARAMETER 1 /* uot::InvalidParameter */
+#define UOT_DEGENERATE_SUM 2    /* uot::DegenerateSum */
+#define UOT_PARTITION_ERROR 3   /* uot::PartitionError */
+#define UOT_CONFIG_ERROR 4      /* uot::ConfigError (launch configuration cannot cover the matrix) */
+#define UOT_CUDA_ERROR 5        /* CUDA runtime failure (no reference analogue) */
+#define UOT_NCCL_ERROR 6        /* NCCL failure (no reference analogue) */
+
+/* Dtype codes: uot::Dtype (include/uot/matrix.hpp:13). Only f32 has a kernel. */
+#define UOT_F32 1
+#define UOT_F64 2
+
+#if defined(__GNUC__)
+#define UOT_API __attribute__((visibility("default")))
+#else
+#define UOT_API
+#endif
+
+typedef struct uot_ctx uot_ctx;
+
+/* Layout and launch facts of a session (for tests, benches and DESIGN.md). */
+typedef struct uot_layout {
+  uint64_t rows;         /* local rows (row block of this rank) */
+  uint64_t cols;         /* logical columns */
+  uint64_t row_offset;   /* first global row of this rank */
+  uint64_t global_rows;
+  uint32_t pitch;        /* floats per device row (>= cols, multiple of 4*G) */
+  uint32_t slice;        /* floats per CTA column slice */
+  uint32_t G;            /* CTAs sharing a row */
+  uint32_t groups;       /* row groups (grid = groups*G) */
+  uint32_t rows_per_step;
+  uint32_t threads;      /* CTA size of the sweep kernel */
+  uint32_t chunks;       /* float4 chunks per thread per row */
+  uint32_t smem_bytes;   /* dynamic shared memory of the sweep kernel */
+  uint32_t nbuf;         /* shared-memory ring slots */
+  uint32_t sms;
+  int32_t rank, nranks, device, evict_first;
+} uot_layout;
+
+/* ---- sessions ---------------------------------------------------------- */
+
+/* New session for a rows x cols problem on `device`. Replaces the problem/plan
+ * copy at the top of fused_solve (fused.hpp:262-272). */
+UOT_API int uot_create(uot_ctx** out, uint64_t rows, uint64_t cols, int dtype, int device);
+
+/* Multi-GPU session: rank `rank` of `nranks` owns the row block
+ * RankPartition::make(nranks, global_rows).blocks[rank] (src/plan.cpp:35-44;
+ * PartitionError when nranks > global_rows) and joins the NCCL communicator
+ * identified by `nccl_id` (128 bytes from uot_nccl_unique_id on rank 0).
+ * Replaces distributed_solve's rank state (distributed.hpp:65-79). */
+UOT_API int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device,
+                    int rank, int nranks, const uint8_t* nccl_id);
+UOT_API int uot_nccl_unique_id(uint8_t* out128);
+
+UOT_API void uot_destroy(uot_ctx* ctx);
+UOT_API const char* uot_last_error(const uot_ctx* ctx);
+UOT_API int uot_get_layout(const uot_ctx* ctx, uot_layout* out);
+/* The CUDA stream every kernel of the session is launched on (cudaStream_t). */
+UOT_API void* uot_get_stream(const uot_ctx* ctx);
+
+/* ---- problem ----------------------------------------------------------- */
+
+/* Upload Problem<float> {a (rows x cols row-major, this rank's rows), rpd
+ * (this rank's rows), cpd (all cols), er, ep} (problem.hpp:19-28) and validate
+ * it like require_valid (problem.hpp:64-103) -> UOT_INVALID_PARAMETER. fi =
+ * compute_fi(er, ep) (scaling.cpp:9-13). Resets the iteration state. */
+UOT_API int uot_set_problem(uot_ctx* ctx, const float* a, const double* rpd, const double* cpd, double er,
+                    double ep);
+/* gen_problem_t<float>(seed, global_rows, cols) (problem_io.hpp:17-31) generated
+ * directly in HBM, bit-identical to the host generator, then er/ep applied. */
+UOT_API int uot_generate_problem(uot_ctx* ctx, uint64_t seed, double er, double ep);
+/* Override the damping exponent (fused_iterate takes fi directly, fused.hpp:165).
+ * fi must lie in (0, 1]. */
+UOT_API int uot_set_fi(uot_ctx* ctx, double fi);
+/* Replace only the plan (the current matrix) of this rank; marginals stay. */
+UOT_API int uot_set_plan(uot_ctx* ctx, const float* a);
+
+/* ---- the path ---------------------------------------------------------- */
+
+/* FusedState{init_col_sums(plan, blocks)} (fused.hpp:96-110, 271): one read
+ * sweep over P, then column factors beta(1). Multi-GPU: the ranks' seeds are
+ * allreduced (distributed.hpp:78 + 88-92). */
+UOT_API int uot_init_col_sums(uot_ctx* ctx);
+/* FusedState given by the caller (fused_iterate's state argument). */
+UOT_API int uot_set_col_sums(uot_ctx* ctx, const double* col_sums);
+UOT_API int uot_get_col_sums(const uot_ctx* ctx, double* out);
+
+/* Run up to k fused iterations on the device (fused_iterate_parallel,
+ * fused.hpp:197-250, one sm_100a sweep kernel + one finalize kernel each),
+ * stopping after the first iteration whose convergence_error <= tol
+ * (fused.hpp:273-281). Outputs: iterations completed by this call, the error of
+ * the last completed iteration, and whether it converged. Use tol = 1e-300 for
+ * fixed-length runs. A degenerate row or column sum returns UOT_DEGENERATE_SUM
+ * (detected on device; the plan is then in an unspecified partially-updated
+ * state, as after the reference's throw). */
+UOT_API int uot_iterate(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations, double* final_error,
+                int* converged);
+
+/* ScalingFactors of the last completed iteration (problem.hpp:30-33); alpha is
+ * this rank's rows, beta all columns. */
+UOT_API int uot_get_factors(const uot_ctx* ctx, double* alpha, double* beta);
+/* The plan (rows x cols row-major) of this rank. */
+UOT_API int uot_get_plan(const uot_ctx* ctx, float* out);
+/* Completed iterations and the error of the last one. */
+UOT_API int uot_get_report(const uot_ctx* ctx, uint64_t* iterations, double* final_error, int* converged);
+/* CommStats (distributed.hpp:24-27). */
+UOT_API int uot_get_comm_stats(const uot_ctx* ctx, uint64_t* allreduce_calls, uint64_t* doubles_reduced);
+
+/* Device time of the sweep / finalize kernels of the last uot_iterate call when
+ * timing is enabled (CUDA events on the session stream around each launch). */
+UOT_API int uot_set_timing(uot_ctx* ctx, int enabled);
+UOT_API int uot_get_timing(const uot_ctx* ctx, double* sweep_ms, double* finalize_ms, uint64_t* sweeps);
+/* Number of kernels this session launched so far (all kinds). */
+UOT_API uint64_t uot_kernel_launches(const uot_ctx* ctx);
+
+/* ---- scalars and plans (host; scaling.cpp:9-29, plan.cpp:11-44) -------- */
+UOT_API int uot_compute_fi(double er, double ep, double* fi);
+UOT_API int uot_rescale_factor(double target, double sum, double fi, double* out);
+UOT_API double uot_convergence_error(const double* alpha, uint64_t m, const double* beta, uint64_t n);
+/* bounds[0..ranks]: rank r owns [bounds[r], bounds[r+1]). */
+UOT_API int uot_rank_partition(uint64_t ranks, uint64_t rows, uint64_t* bounds);
+/* gen_problem_t<float> on the host (threads > 1 fills A in parallel). */
+UOT_API int uot_gen_problem_f32(uint64_t seed, uint64_t m, uint64_t n, float* a, double* rpd, double* cpd,
+                        int threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UOT_CUDA_H */

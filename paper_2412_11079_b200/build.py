@@ -1,0 +1,55 @@
+"""Build the sm_100a extension in-tree: paper_2412_11079_b200/libuot_cuda.so.
+
+nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3, C-ABI shared
+library (include/uot_cuda.h), cudart static, NCCL loaded lazily with dlopen.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+SO = os.path.join(PKG, "libuot_cuda.so")
+SOURCES = [os.path.join(CSRC, "uot_cuda.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")] + [
+    os.path.join(ROOT, "include", "uot_cuda.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def nvcc_cmd(out: str = SO, extra: list[str] | None = None) -> list[str]:
+    return [
+        NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+        "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+        "-Xptxas", "-v", "--expt-relaxed-constexpr",
+        "-I", os.path.join(ROOT, "include"),
+        *(extra or []), "-o", out, *SOURCES, "-ldl", "-lpthread",
+    ]
+
+
+def stale() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    return any(os.path.getmtime(d) > t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or stale():
+        cmd = nvcc_cmd()
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        log = r.stdout + r.stderr
+        with open(os.path.join(PKG, "build.log"), "w") as f:
+            f.write(" ".join(cmd) + "\n" + log)
+        if r.returncode != 0:
+            sys.stderr.write(log)
+            raise RuntimeError("nvcc failed building libuot_cuda.so (see build.log)")
+        if verbose:
+            sys.stderr.write(log)
+    return SO
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

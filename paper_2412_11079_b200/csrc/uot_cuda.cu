@@ -1,0 +1,749 @@
+// uot_cuda.cu — host runtime of the B200-native fused Sinkhorn-UOT path and its
+// C ABI (include/uot_cuda.h). One session = one problem resident in HBM on one
+// GPU (or one rank's row block of it), driven on one CUDA stream.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/uot_cuda.h"
+#include "finalize.cuh"
+#include "problem.cuh"
+#include "sweep.cuh"
+
+using namespace uotk;
+
+namespace {
+
+constexpr int kNbuf = 6;            // shared-memory ring slots of the sweep
+constexpr unsigned kSliceMax = 8192;  // floats of a row one CTA owns (32 KiB)
+
+// ------------------------------------------------------------ kernel table --
+using SweepFn = void (*)(const SweepArgs);
+struct SweepCfg {
+  int nt, v, bm;
+  SweepFn iter, iter_x, seed;
+};
+
+template <int NT, int V, int BM, bool HAS_X>
+SweepCfg make_cfg() {
+  SweepCfg c{NT, V, BM, sweep_kernel<NT, V, BM, kNbuf, false, false>, nullptr,
+             sweep_kernel<NT, V, BM, kNbuf, false, true>};
+  if constexpr (HAS_X) c.iter_x = sweep_kernel<NT, V, BM, kNbuf, true, false>;
+  return c;
+}
+
+const std::vector<SweepCfg>& cfg_table() {
+  static const std::vector<SweepCfg> t = {
+      make_cfg<128, 1, 4, false>(), make_cfg<256, 1, 8, false>(), make_cfg<512, 1, 4, false>(),
+      make_cfg<512, 2, 2, true>(),  make_cfg<512, 3, 1, true>(),  make_cfg<512, 4, 1, true>(),
+  };
+  return t;
+}
+
+// ------------------------------------------------------------------- NCCL --
+// Loaded on first multi-GPU use so single-GPU sessions never touch libnccl.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+  std::string err;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.CommDestroy && a.GetErrorString;
+    if (!a.ok) a.err = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+unsigned round_up(unsigned x, unsigned m) { return (x + m - 1) / m * m; }
+
+void balanced_bounds(uint64_t k, uint64_t rows, uint64_t* bounds) {  // plan.cpp:11-21
+  const uint64_t base = rows / k, rem = rows % k;
+  bounds[0] = 0;
+  for (uint64_t w = 0; w < k; ++w) bounds[w + 1] = bounds[w] + base + (w < rem ? 1 : 0);
+}
+
+struct Status {
+  int code;
+  std::string msg;
+};
+
+}  // namespace
+
+struct uot_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sms = 0;
+  uint64_t rows = 0, cols = 0, row_offset = 0, global_rows = 0;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+
+  // layout
+  unsigned G = 1, slice = 0, pitch = 0, groups = 1, B = 1, buf_stride = 0, grid = 1;
+  size_t smem = 0;
+  const SweepCfg* cfg = nullptr;
+  int evict_first = 0;
+
+  // device buffers
+  float* P = nullptr;
+  double *rpd = nullptr, *cpd = nullptr, *alpha = nullptr, *beta2 = nullptr, *col_sums = nullptr,
+         *xsum = nullptr, *partials = nullptr, *cta_err = nullptr, *xval = nullptr;
+  unsigned long long* xflag = nullptr;
+  Control* ctl = nullptr;
+  int* dflag = nullptr;
+  Control* h_ctl = nullptr;  // pinned mirror
+
+  double fi = 0.0;
+  bool have_problem = false, seeded = false;
+
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  double sweep_ms = 0.0, fin_ms = 0.0;
+  uint64_t sweeps_timed = 0;
+  uint64_t launches = 0;
+
+  std::string last_error;
+
+  int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    last_error = buf;
+    return code;
+  }
+  int cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return UOT_OK;
+    return fail(UOT_CUDA_ERROR, "%s: %s", what, cudaGetErrorString(e));
+  }
+};
+
+#define CK(expr)                                              \
+  do {                                                        \
+    const int _rc = ctx->cuda((expr), #expr);                 \
+    if (_rc != UOT_OK) return _rc;                            \
+  } while (0)
+
+namespace {
+
+int plan_layout(uot_ctx* ctx) {
+  const uint64_t cols = ctx->cols;
+  if (cols > (1ull << 26)) return ctx->fail(UOT_CONFIG_ERROR, "cols %llu too large", (unsigned long long)cols);
+  unsigned G = cols <= kSliceMax ? 1u : static_cast<unsigned>((cols + kSliceMax - 1) / kSliceMax);
+  if (G > static_cast<unsigned>(ctx->sms) || G > 32)
+    return ctx->fail(UOT_CONFIG_ERROR, "cols %llu needs %u CTAs per row (max %d)",
+                     (unsigned long long)cols, G, std::min(ctx->sms, 32));
+  const unsigned slice = round_up(static_cast<unsigned>((cols + G - 1) / G), 4);
+  const SweepCfg* cfg = nullptr;
+  for (const auto& c : cfg_table())
+    if (static_cast<unsigned>(c.nt * 4 * c.v) >= slice && (G == 1 || c.iter_x)) {
+      cfg = &c;
+      break;
+    }
+  if (!cfg) return ctx->fail(UOT_CONFIG_ERROR, "no sweep configuration covers a %u-float slice", slice);
+  ctx->G = G;
+  ctx->slice = slice;
+  ctx->pitch = slice * G;
+  ctx->cfg = cfg;
+  ctx->B = std::max(1u, std::min(static_cast<unsigned>(cfg->bm), kSliceMax / slice));
+  ctx->groups = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->rows, ctx->sms / G)));
+  ctx->grid = ctx->groups * G;
+  ctx->buf_stride = round_up(ctx->B * slice * 4u, 128);
+  const int nw = cfg->nt / 32;
+  ctx->smem = static_cast<size_t>(kNbuf) * ctx->buf_stride + kNbuf * 8 +
+              (2 * nw * cfg->bm + 2 * cfg->bm + nw) * sizeof(double);
+  ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * 4 > (64ull << 20) ? 1 : 0;
+  for (SweepFn fn : {cfg->iter, cfg->iter_x, cfg->seed}) {
+    if (!fn) continue;
+    const int rc = ctx->cuda(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(ctx->smem)),
+                             "cudaFuncSetAttribute(smem)");
+    if (rc) return rc;
+  }
+  return UOT_OK;
+}
+
+template <typename T>
+int dalloc(uot_ctx* ctx, T** p, size_t count) {
+  return ctx->cuda(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)),
+                   "cudaMalloc");
+}
+
+int alloc_all(uot_ctx* ctx) {
+  const size_t rows = ctx->rows, pitch = ctx->pitch;
+  int rc;
+  if ((rc = dalloc(ctx, &ctx->P, rows * pitch))) return rc;
+  if ((rc = dalloc(ctx, &ctx->rpd, rows))) return rc;
+  if ((rc = dalloc(ctx, &ctx->alpha, rows))) return rc;
+  if ((rc = dalloc(ctx, &ctx->cpd, pitch))) return rc;
+  if ((rc = dalloc(ctx, &ctx->beta2, 2 * pitch))) return rc;
+  if ((rc = dalloc(ctx, &ctx->col_sums, pitch))) return rc;
+  if ((rc = dalloc(ctx, &ctx->xsum, pitch + ctx->nranks))) return rc;
+  if ((rc = dalloc(ctx, &ctx->partials, static_cast<size_t>(ctx->groups) * pitch))) return rc;
+  if ((rc = dalloc(ctx, &ctx->cta_err, ctx->grid))) return rc;
+  const size_t xn = static_cast<size_t>(ctx->grid) * kRing * ctx->cfg->bm;
+  if ((rc = dalloc(ctx, &ctx->xval, xn))) return rc;
+  if ((rc = dalloc(ctx, &ctx->xflag, xn))) return rc;
+  if ((rc = dalloc(ctx, &ctx->ctl, 1))) return rc;
+  if ((rc = dalloc(ctx, &ctx->dflag, 1))) return rc;
+  if ((rc = ctx->cuda(cudaMallocHost(&ctx->h_ctl, sizeof(Control)), "cudaMallocHost"))) return rc;
+  CK(cudaMemsetAsync(ctx->xflag, 0, xn * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), ctx->stream));
+  CK(cudaMemsetAsync(ctx->beta2, 0, 2 * pitch * sizeof(double), ctx->stream));
+  CK(cudaMemsetAsync(ctx->cpd, 0, pitch * sizeof(double), ctx->stream));
+  return UOT_OK;
+}
+
+int create_common(uot_ctx* ctx, int device) {
+  ctx->device = device;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return ctx->fail(UOT_INVALID_PARAMETER, "device %d out of range (%d visible)", device, ndev);
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  int rc = plan_layout(ctx);
+  if (rc) return rc;
+  return alloc_all(ctx);
+}
+
+SweepArgs sweep_args(const uot_ctx* ctx) {
+  SweepArgs a;
+  a.P = ctx->P;
+  a.beta2 = ctx->beta2;
+  a.rpd = ctx->rpd;
+  a.alpha = ctx->alpha;
+  a.partials = ctx->partials;
+  a.cta_err = ctx->cta_err;
+  a.xval = ctx->xval;
+  a.xflag = ctx->xflag;
+  a.ctl = ctx->ctl;
+  a.rows = ctx->rows;
+  a.pitch = ctx->pitch;
+  a.slice = ctx->slice;
+  a.G = ctx->G;
+  a.groups = ctx->groups;
+  a.B = ctx->B;
+  a.buf_stride = ctx->buf_stride;
+  a.evict_first = ctx->evict_first;
+  a.fi = ctx->fi;
+  return a;
+}
+
+FinalizeArgs fin_args(const uot_ctx* ctx) {
+  FinalizeArgs f;
+  f.partials = ctx->partials;
+  f.cta_err = ctx->cta_err;
+  f.cpd = ctx->cpd;
+  f.beta2 = ctx->beta2;
+  f.col_sums = ctx->col_sums;
+  f.xsum = ctx->xsum;
+  f.ctl = ctx->ctl;
+  f.cols = static_cast<unsigned>(ctx->cols);
+  f.pitch = ctx->pitch;
+  f.groups = ctx->groups;
+  f.grid = ctx->grid;
+  f.rank = static_cast<unsigned>(ctx->rank);
+  f.nranks = static_cast<unsigned>(ctx->nranks);
+  f.fi = ctx->fi;
+  return f;
+}
+
+int launch_sweep(uot_ctx* ctx, bool seed) {
+  const SweepArgs a = sweep_args(ctx);
+  const bool xchg = !seed && ctx->G > 1;
+  SweepFn fn = seed ? ctx->cfg->seed : (xchg ? ctx->cfg->iter_x : ctx->cfg->iter);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(ctx->grid);
+  lc.blockDim = dim3(ctx->cfg->nt);
+  lc.dynamicSmemBytes = ctx->smem;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // CTAs of a group spin on each other
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = xchg ? 1 : 0;
+  ctx->launches++;
+  return ctx->cuda(cudaLaunchKernelEx(&lc, fn, a), "sweep launch");
+}
+
+template <int MODE>
+int launch_finalize_single(uot_ctx* ctx) {
+  const unsigned blocks = (ctx->pitch + 255) / 256;
+  ctx->launches++;
+  finalize_kernel<MODE, true, true><<<blocks, 256, 0, ctx->stream>>>(fin_args(ctx));
+  return ctx->cuda(cudaGetLastError(), "finalize launch");
+}
+
+int nccl_check(uot_ctx* ctx, ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return UOT_OK;
+  return ctx->fail(UOT_NCCL_ERROR, "%s: %s", what, nccl().GetErrorString(r));
+}
+
+// Multi-GPU tail: local reduce -> one allreduce of cols + nranks doubles -> beta.
+template <int MODE>
+int launch_finalize_dist(uot_ctx* ctx) {
+  const unsigned blocks = (ctx->pitch + 255) / 256;
+  const FinalizeArgs f = fin_args(ctx);
+  ctx->launches += 2;
+  finalize_kernel<MODE, true, false><<<blocks, 256, 0, ctx->stream>>>(f);
+  int rc = ctx->cuda(cudaGetLastError(), "finalize(reduce) launch");
+  if (rc) return rc;
+  rc = nccl_check(ctx, nccl().AllReduce(ctx->xsum, ctx->xsum, ctx->cols + ctx->nranks, ncclFloat64,
+                                        ncclSum, ctx->comm, ctx->stream),
+                  "ncclAllReduce");
+  if (rc) return rc;
+  finalize_kernel<MODE, false, true><<<blocks, 256, 0, ctx->stream>>>(f);
+  return ctx->cuda(cudaGetLastError(), "finalize(beta) launch");
+}
+
+template <int MODE>
+int launch_finalize(uot_ctx* ctx) {
+  return ctx->nranks > 1 ? launch_finalize_dist<MODE>(ctx) : launch_finalize_single<MODE>(ctx);
+}
+
+int sync_ctl(uot_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(Control), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return UOT_OK;
+}
+
+int status_of(uot_ctx* ctx) {
+  const int st = ctx->h_ctl->status;
+  if (st & kStatusExchangeTimeout)
+    return ctx->fail(UOT_CUDA_ERROR, "row-sum exchange timed out (CTAs not co-resident)");
+  if (st & (kStatusDegenerateAlpha | kStatusDegenerateBeta))
+    return ctx->fail(UOT_DEGENERATE_SUM, "rescale_factor: %s",
+                     (st & kStatusDegenerateAlpha) ? "a row sum is not strictly positive or its factor left the positive finite range"
+                                                   : "a column sum is not strictly positive or its factor left the positive finite range");
+  return UOT_OK;
+}
+
+int check_marginals(uot_ctx* ctx, const double* rpd, const double* cpd, double er, double ep) {
+  for (uint64_t i = 0; i < ctx->rows; ++i)
+    if (!(rpd[i] > 0.0) || !std::isfinite(rpd[i]))
+      return ctx->fail(UOT_INVALID_PARAMETER, "row marginal %llu is not strictly positive",
+                       (unsigned long long)(i + ctx->row_offset));
+  for (uint64_t j = 0; j < ctx->cols; ++j)
+    if (!(cpd[j] > 0.0) || !std::isfinite(cpd[j]))
+      return ctx->fail(UOT_INVALID_PARAMETER, "column marginal %llu is not strictly positive",
+                       (unsigned long long)j);
+  if (uot_compute_fi(er, ep, &ctx->fi) != UOT_OK)
+    return ctx->fail(UOT_INVALID_PARAMETER, "er must be positive and finite, ep non-negative and finite");
+  return UOT_OK;
+}
+
+int after_matrix_upload(uot_ctx* ctx) {
+  const unsigned gblocks = static_cast<unsigned>(ctx->sms) * 8;
+  if (ctx->pitch > ctx->cols) {
+    zero_padding_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->P, ctx->rows, static_cast<unsigned>(ctx->cols), ctx->pitch);
+    ctx->launches++;
+  }
+  CK(cudaMemsetAsync(ctx->dflag, 0, sizeof(int), ctx->stream));
+  validate_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->P, ctx->rows, static_cast<unsigned>(ctx->cols), ctx->pitch, ctx->dflag);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, ctx->dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (bad) return ctx->fail(UOT_INVALID_PARAMETER, "matrix entry is not strictly positive");
+  return UOT_OK;
+}
+
+int reset_state(uot_ctx* ctx) {
+  reset_control_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctl);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  ctx->seeded = false;
+  return UOT_OK;
+}
+
+void record(uot_ctx* ctx, size_t idx) {
+  while (ctx->ev.size() <= idx) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->ev.push_back(e);
+  }
+  cudaEventRecord(ctx->ev[idx], ctx->stream);
+}
+
+}  // namespace
+
+// ============================================================== C ABI ====
+extern "C" {
+
+int uot_create(uot_ctx** out, uint64_t rows, uint64_t cols, int dtype, int device) {
+  if (!out) return UOT_INVALID_PARAMETER;
+  *out = nullptr;
+  auto* ctx = new uot_ctx();
+  *out = ctx;
+  if (rows < 1 || cols < 1) return ctx->fail(UOT_INVALID_PARAMETER, "matrix must be at least 1x1");
+  if (dtype != UOT_F32)
+    return ctx->fail(UOT_INVALID_PARAMETER, "dtype %d: only f32 (Dtype::f32) has an sm_100a kernel", dtype);
+  ctx->rows = ctx->global_rows = rows;
+  ctx->cols = cols;
+  return create_common(ctx, device);
+}
+
+int uot_nccl_unique_id(uint8_t* out128) {
+  if (!nccl().ok) return UOT_NCCL_ERROR;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return UOT_NCCL_ERROR;
+  static_assert(sizeof(id.internal) == 128, "nccl id size");
+  std::memcpy(out128, id.internal, 128);
+  return UOT_OK;
+}
+
+int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device,
+                    int rank, int nranks, const uint8_t* nccl_id) {
+  if (!out) return UOT_INVALID_PARAMETER;
+  *out = nullptr;
+  auto* ctx = new uot_ctx();
+  *out = ctx;
+  if (global_rows < 1 || cols < 1) return ctx->fail(UOT_INVALID_PARAMETER, "matrix must be at least 1x1");
+  if (dtype != UOT_F32)
+    return ctx->fail(UOT_INVALID_PARAMETER, "dtype %d: only f32 (Dtype::f32) has an sm_100a kernel", dtype);
+  if (nranks < 1 || static_cast<uint64_t>(nranks) > global_rows)  // plan.cpp:36-39
+    return ctx->fail(UOT_PARTITION_ERROR, "RankPartition: %d ranks for %llu rows would leave a rank without rows",
+                     nranks, (unsigned long long)global_rows);
+  if (rank < 0 || rank >= nranks) return ctx->fail(UOT_PARTITION_ERROR, "rank %d outside [0,%d)", rank, nranks);
+  std::vector<uint64_t> b(nranks + 1);
+  balanced_bounds(nranks, global_rows, b.data());
+  ctx->global_rows = global_rows;
+  ctx->row_offset = b[rank];
+  ctx->rows = b[rank + 1] - b[rank];
+  ctx->cols = cols;
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  int rc = create_common(ctx, device);
+  if (rc) return rc;
+  if (nranks > 1) {
+    if (!nccl().ok) return ctx->fail(UOT_NCCL_ERROR, "%s", nccl().err.c_str());
+    ncclUniqueId id;
+    std::memcpy(id.internal, nccl_id, 128);
+    rc = nccl_check(ctx, nccl().CommInitRank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+    if (rc) return rc;
+  }
+  return UOT_OK;
+}
+
+void uot_destroy(uot_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+  }
+  if (ctx->comm) nccl().CommDestroy(ctx->comm);
+  for (auto e : ctx->ev) cudaEventDestroy(e);
+  void* bufs[] = {ctx->P,     ctx->rpd,   ctx->cpd,      ctx->alpha,   ctx->beta2, ctx->col_sums, ctx->xsum,
+                  ctx->partials, ctx->cta_err, ctx->xval, ctx->xflag, ctx->ctl, ctx->dflag};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* uot_last_error(const uot_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null session"; }
+
+int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
+  if (!ctx || !o || !ctx->cfg) return UOT_INVALID_PARAMETER;
+  o->rows = ctx->rows;
+  o->cols = ctx->cols;
+  o->row_offset = ctx->row_offset;
+  o->global_rows = ctx->global_rows;
+  o->pitch = ctx->pitch;
+  o->slice = ctx->slice;
+  o->G = ctx->G;
+  o->groups = ctx->groups;
+  o->rows_per_step = ctx->B;
+  o->threads = ctx->cfg->nt;
+  o->chunks = ctx->cfg->v;
+  o->smem_bytes = static_cast<uint32_t>(ctx->smem);
+  o->nbuf = kNbuf;
+  o->sms = ctx->sms;
+  o->rank = ctx->rank;
+  o->nranks = ctx->nranks;
+  o->device = ctx->device;
+  o->evict_first = ctx->evict_first;
+  return UOT_OK;
+}
+
+void* uot_get_stream(const uot_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int uot_set_problem(uot_ctx* ctx, const float* a, const double* rpd, const double* cpd, double er,
+                    double ep) {
+  if (!ctx || !a || !rpd || !cpd) return UOT_INVALID_PARAMETER;
+  CK(cudaSetDevice(ctx->device));
+  int rc = check_marginals(ctx, rpd, cpd, er, ep);
+  if (rc) return rc;
+  ctx->have_problem = false;
+  CK(cudaMemcpy2DAsync(ctx->P, ctx->pitch * sizeof(float), a, ctx->cols * sizeof(float),
+                       ctx->cols * sizeof(float), ctx->rows, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->rpd, rpd, ctx->rows * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->cpd, cpd, ctx->cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  if ((rc = reset_state(ctx))) return rc;
+  if ((rc = after_matrix_upload(ctx))) return rc;
+  ctx->have_problem = true;
+  return UOT_OK;
+}
+
+int uot_generate_problem(uot_ctx* ctx, uint64_t seed, double er, double ep) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  CK(cudaSetDevice(ctx->device));
+  if (uot_compute_fi(er, ep, &ctx->fi) != UOT_OK)
+    return ctx->fail(UOT_INVALID_PARAMETER, "er must be positive and finite, ep non-negative and finite");
+  ctx->have_problem = false;
+  const unsigned gblocks = static_cast<unsigned>(ctx->sms) * 16;
+  gen_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->P, seed, ctx->row_offset, ctx->rows,
+                                                     static_cast<unsigned>(ctx->cols), ctx->pitch);
+  gen_marginals_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->rpd, ctx->cpd, seed, ctx->global_rows,
+                                                         ctx->row_offset, ctx->rows,
+                                                         static_cast<unsigned>(ctx->cols));
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  int rc = reset_state(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->have_problem = true;
+  return UOT_OK;
+}
+
+int uot_set_fi(uot_ctx* ctx, double fi) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  if (!(fi > 0.0) || !(fi <= 1.0)) return ctx->fail(UOT_INVALID_PARAMETER, "fi must lie in (0, 1]");
+  ctx->fi = fi;
+  return UOT_OK;
+}
+
+int uot_set_plan(uot_ctx* ctx, const float* a) {
+  if (!ctx || !a) return UOT_INVALID_PARAMETER;
+  if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpy2DAsync(ctx->P, ctx->pitch * sizeof(float), a, ctx->cols * sizeof(float),
+                       ctx->cols * sizeof(float), ctx->rows, cudaMemcpyHostToDevice, ctx->stream));
+  return after_matrix_upload(ctx);
+}
+
+int uot_init_col_sums(uot_ctx* ctx) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
+  CK(cudaSetDevice(ctx->device));
+  int rc = reset_state(ctx);
+  if (rc) return rc;
+  if ((rc = launch_sweep(ctx, /*seed=*/true))) return rc;
+  if ((rc = launch_finalize<kFinSeed>(ctx))) return rc;
+  if ((rc = sync_ctl(ctx))) return rc;
+  ctx->seeded = true;
+  return UOT_OK;
+}
+
+int uot_set_col_sums(uot_ctx* ctx, const double* col_sums) {
+  if (!ctx || !col_sums) return UOT_INVALID_PARAMETER;
+  if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(ctx->col_sums, col_sums, ctx->cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  // Recompute beta(iter+1) from the given state; its error slot starts at zero.
+  CK(cudaMemsetAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Control, err_beta), 0,
+                     2 * sizeof(double), ctx->stream));
+  const unsigned blocks = (ctx->pitch + 255) / 256;
+  ctx->launches++;
+  finalize_kernel<kFinBetaOnly, false, true><<<blocks, 256, 0, ctx->stream>>>(fin_args(ctx));
+  CK(cudaGetLastError());
+  int rc = sync_ctl(ctx);
+  if (rc) return rc;
+  ctx->seeded = true;
+  return UOT_OK;
+}
+
+int uot_get_col_sums(const uot_ctx* cctx, double* out) {
+  auto* ctx = const_cast<uot_ctx*>(cctx);
+  if (!ctx || !out) return UOT_INVALID_PARAMETER;
+  if (!ctx->seeded) return ctx->fail(UOT_INVALID_PARAMETER, "no carried column sums (call init_col_sums)");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(out, ctx->col_sums, ctx->cols * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return UOT_OK;
+}
+
+int uot_iterate(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations, double* final_error,
+                int* converged) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
+  if (!ctx->seeded)
+    return ctx->fail(UOT_INVALID_PARAMETER, "carried column sums missing (call init_col_sums)");
+  if (!(tol > 0.0)) return ctx->fail(UOT_INVALID_PARAMETER, "tol must be positive");
+  if (k < 1) return ctx->fail(UOT_INVALID_PARAMETER, "max_iter must be at least 1");
+  CK(cudaSetDevice(ctx->device));
+  const uint64_t before = ctx->h_ctl->iter;
+  begin_iterate_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctl, tol);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  int rc;
+  for (uint64_t i = 0; i < k; ++i) {
+    if (ctx->timing) record(ctx, 3 * i);
+    if ((rc = launch_sweep(ctx, false))) return rc;
+    if (ctx->timing) record(ctx, 3 * i + 1);
+    if ((rc = launch_finalize<kFinIter>(ctx))) return rc;
+    if (ctx->timing) record(ctx, 3 * i + 2);
+  }
+  if ((rc = sync_ctl(ctx))) return rc;
+  if (ctx->timing) {
+    ctx->sweep_ms = ctx->fin_ms = 0.0;
+    for (uint64_t i = 0; i < k; ++i) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, ctx->ev[3 * i], ctx->ev[3 * i + 1]);
+      cudaEventElapsedTime(&b, ctx->ev[3 * i + 1], ctx->ev[3 * i + 2]);
+      ctx->sweep_ms += a;
+      ctx->fin_ms += b;
+    }
+    ctx->sweeps_timed = k;
+  }
+  if (iterations) *iterations = ctx->h_ctl->iter - before;
+  if (final_error) *final_error = ctx->h_ctl->last_error;
+  if (converged) *converged = ctx->h_ctl->converged;
+  return status_of(ctx);
+}
+
+int uot_get_factors(const uot_ctx* cctx, double* alpha, double* beta) {
+  auto* ctx = const_cast<uot_ctx*>(cctx);
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  const uint64_t it = ctx->h_ctl ? ctx->h_ctl->iter : 0;
+  if (it == 0) return ctx->fail(UOT_INVALID_PARAMETER, "no completed iteration");
+  CK(cudaSetDevice(ctx->device));
+  if (alpha)
+    CK(cudaMemcpyAsync(alpha, ctx->alpha, ctx->rows * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (beta)
+    CK(cudaMemcpyAsync(beta, ctx->beta2 + (it & 1ull) * ctx->pitch, ctx->cols * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return UOT_OK;
+}
+
+int uot_get_plan(const uot_ctx* cctx, float* out) {
+  auto* ctx = const_cast<uot_ctx*>(cctx);
+  if (!ctx || !out) return UOT_INVALID_PARAMETER;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpy2DAsync(out, ctx->cols * sizeof(float), ctx->P, ctx->pitch * sizeof(float),
+                       ctx->cols * sizeof(float), ctx->rows, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return UOT_OK;
+}
+
+int uot_get_report(const uot_ctx* ctx, uint64_t* iterations, double* final_error, int* converged) {
+  if (!ctx || !ctx->h_ctl) return UOT_INVALID_PARAMETER;
+  if (iterations) *iterations = ctx->h_ctl->iter;
+  if (final_error) *final_error = ctx->h_ctl->last_error;
+  if (converged) *converged = ctx->h_ctl->converged;
+  return UOT_OK;
+}
+
+int uot_get_comm_stats(const uot_ctx* ctx, uint64_t* calls, uint64_t* doubles) {
+  if (!ctx || !ctx->h_ctl) return UOT_INVALID_PARAMETER;
+  // One allreduce of the column vector per completed iteration (distributed.hpp:88-94).
+  const uint64_t it = ctx->nranks > 1 ? ctx->h_ctl->iter : 0;
+  if (calls) *calls = it;
+  if (doubles) *doubles = it * ctx->cols;
+  return UOT_OK;
+}
+
+int uot_set_timing(uot_ctx* ctx, int enabled) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  ctx->timing = enabled != 0;
+  return UOT_OK;
+}
+
+int uot_get_timing(const uot_ctx* ctx, double* sweep_ms, double* finalize_ms, uint64_t* sweeps) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  if (sweep_ms) *sweep_ms = ctx->sweep_ms;
+  if (finalize_ms) *finalize_ms = ctx->fin_ms;
+  if (sweeps) *sweeps = ctx->sweeps_timed;
+  return UOT_OK;
+}
+
+uint64_t uot_kernel_launches(const uot_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ------------------------------------------------------------ host scalars --
+int uot_compute_fi(double er, double ep, double* fi) {  // scaling.cpp:9-13
+  if (!(er > 0.0) || !std::isfinite(er)) return UOT_INVALID_PARAMETER;
+  if (!(ep >= 0.0) || !std::isfinite(ep)) return UOT_INVALID_PARAMETER;
+  *fi = er / (er + ep);
+  return UOT_OK;
+}
+
+int uot_rescale_factor(double target, double sum, double fi, double* out) {  // scaling.cpp:15-22
+  if (!(sum > 0.0)) return UOT_DEGENERATE_SUM;
+  const double f = std::pow(target / sum, fi);
+  if (!(f > 0.0) || !std::isfinite(f)) return UOT_DEGENERATE_SUM;
+  *out = f;
+  return UOT_OK;
+}
+
+double uot_convergence_error(const double* alpha, uint64_t m, const double* beta, uint64_t n) {
+  double e = 0.0;  // scaling.cpp:24-29
+  for (uint64_t i = 0; i < m; ++i) e = std::max(e, std::abs(alpha[i] - 1.0));
+  for (uint64_t j = 0; j < n; ++j) e = std::max(e, std::abs(beta[j] - 1.0));
+  return e;
+}
+
+int uot_rank_partition(uint64_t ranks, uint64_t rows, uint64_t* bounds) {  // plan.cpp:35-44
+  if (ranks < 1 || ranks > rows) return UOT_PARTITION_ERROR;
+  balanced_bounds(ranks, rows, bounds);
+  return UOT_OK;
+}
+
+int uot_gen_problem_f32(uint64_t seed, uint64_t m, uint64_t n, float* a, double* rpd, double* cpd,
+                        int threads) {  // problem_io.hpp:17-31
+  if (m < 1 || n < 1) return UOT_INVALID_PARAMETER;
+  auto unit_at = [seed](uint64_t k) {
+    uint64_t z = seed + (k + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return static_cast<double>((z >> 11) + 1) * 0x1p-53;
+  };
+  const uint64_t mn = m * n;
+  const int nt = std::max(1, std::min<int>(threads, 256));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (uint64_t k = mn * t / nt; k < mn * (t + 1) / nt; ++k) a[k] = static_cast<float>(unit_at(k));
+    });
+  for (auto& x : th) x.join();
+  for (uint64_t i = 0; i < m; ++i) rpd[i] = unit_at(mn + i);
+  for (uint64_t j = 0; j < n; ++j) cpd[j] = unit_at(mn + m + j);
+  return UOT_OK;
+}
+
+}  // extern "C"

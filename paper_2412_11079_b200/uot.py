@@ -1,0 +1,453 @@
+"""Python mirror of the reference solver API (namespace uot), backed by the
+sm_100a extension through its C ABI (include/uot_cuda.h).
+
+Names, argument meaning and errors follow /root/reference/proj/core/include/uot:
+
+  ==========================  =============================================
+  here                        reference
+  ==========================  =============================================
+  Problem                     Problem<T>            problem.hpp:19-28
+  ScalingFactors              ScalingFactors        problem.hpp:30-33
+  SolveReport / SolveResult   problem.hpp:35-48
+  FusedState                  FusedState            fused.hpp:19-23
+  RankPartition.make          RankPartition::make   plan.cpp:35-44
+  compute_fi / rescale_factor / convergence_error   scaling.cpp:9-29
+  gen_problem_t               problem_io.hpp:17-31
+  init_col_sums               fused.hpp:96-110
+  fused_iterate               fused.hpp:164-191 / 197-250
+  fused_solve                 fused.hpp:259-291
+  Session                     (device-resident form of the loop above)
+  Error, InvalidParameter, DegenerateSum, ConfigError, PartitionError
+                              error.hpp:9-37
+  ==========================  =============================================
+
+There is no CPU fallback: importing this module without the built extension,
+or using it without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import build as _build
+
+# ----------------------------------------------------------------- errors --
+
+
+class Error(RuntimeError):
+    """uot::Error (error.hpp:9-12)."""
+
+
+class InvalidParameter(Error):
+    """uot::InvalidParameter (error.hpp:14-17)."""
+
+
+class DegenerateSum(Error):
+    """uot::DegenerateSum (error.hpp:19-23)."""
+
+
+class PartitionError(Error):
+    """uot::PartitionError (error.hpp:29-32)."""
+
+
+class ConfigError(Error):
+    """uot::ConfigError (error.hpp:24-27): the launch cannot cover the matrix."""
+
+
+class CudaError(Error):
+    """CUDA / NCCL runtime failure (no reference analogue)."""
+
+
+class CudaExtensionMissing(ImportError):
+    """The sm_100a extension is not built; there is deliberately no fallback."""
+
+
+_ERRORS = {1: InvalidParameter, 2: DegenerateSum, 3: PartitionError, 4: ConfigError,
+           5: CudaError, 6: CudaError}
+
+UOT_F32, UOT_F64 = 1, 2
+
+# ---------------------------------------------------------------- library --
+
+
+class Layout(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("row_offset", C.c_uint64),
+                ("global_rows", C.c_uint64), ("pitch", C.c_uint32), ("slice", C.c_uint32),
+                ("G", C.c_uint32), ("groups", C.c_uint32), ("rows_per_step", C.c_uint32),
+                ("threads", C.c_uint32), ("chunks", C.c_uint32), ("smem_bytes", C.c_uint32),
+                ("nbuf", C.c_uint32), ("sms", C.c_uint32), ("rank", C.c_int32),
+                ("nranks", C.c_int32), ("device", C.c_int32), ("evict_first", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+_P = C.c_void_p
+_u64, _d, _i = C.c_uint64, C.c_double, C.c_int
+
+
+def lib():
+    """Load libuot_cuda.so (built in-tree). Raises CudaExtensionMissing if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.SO
+    if not os.path.exists(path):
+        if os.environ.get("UOT_AUTOBUILD", "1") == "1":
+            try:
+                _build.build()
+            except Exception as e:  # noqa: BLE001
+                raise CudaExtensionMissing(f"building {path} failed: {e}") from e
+        else:
+            raise CudaExtensionMissing(f"{path} is not built (python -m paper_2412_11079_b200.build)")
+    L = C.CDLL(path)
+    L.uot_create.argtypes = [C.POINTER(_P), _u64, _u64, _i, _i]
+    L.uot_create_dist.argtypes = [C.POINTER(_P), _u64, _u64, _i, _i, _i, _i, _P]
+    L.uot_nccl_unique_id.argtypes = [_P]
+    L.uot_destroy.argtypes = [_P]
+    L.uot_destroy.restype = None
+    L.uot_last_error.argtypes = [_P]
+    L.uot_last_error.restype = C.c_char_p
+    L.uot_get_layout.argtypes = [_P, C.POINTER(Layout)]
+    L.uot_get_stream.argtypes = [_P]
+    L.uot_get_stream.restype = _P
+    L.uot_set_problem.argtypes = [_P, _P, _P, _P, _d, _d]
+    L.uot_generate_problem.argtypes = [_P, _u64, _d, _d]
+    L.uot_set_plan.argtypes = [_P, _P]
+    L.uot_set_fi.argtypes = [_P, _d]
+    L.uot_init_col_sums.argtypes = [_P]
+    L.uot_set_col_sums.argtypes = [_P, _P]
+    L.uot_get_col_sums.argtypes = [_P, _P]
+    L.uot_iterate.argtypes = [_P, _u64, _d, C.POINTER(_u64), C.POINTER(_d), C.POINTER(_i)]
+    L.uot_get_factors.argtypes = [_P, _P, _P]
+    L.uot_get_plan.argtypes = [_P, _P]
+    L.uot_get_report.argtypes = [_P, C.POINTER(_u64), C.POINTER(_d), C.POINTER(_i)]
+    L.uot_get_comm_stats.argtypes = [_P, C.POINTER(_u64), C.POINTER(_u64)]
+    L.uot_set_timing.argtypes = [_P, _i]
+    L.uot_get_timing.argtypes = [_P, C.POINTER(_d), C.POINTER(_d), C.POINTER(_u64)]
+    L.uot_kernel_launches.argtypes = [_P]
+    L.uot_kernel_launches.restype = _u64
+    L.uot_compute_fi.argtypes = [_d, _d, C.POINTER(_d)]
+    L.uot_rescale_factor.argtypes = [_d, _d, _d, C.POINTER(_d)]
+    L.uot_convergence_error.argtypes = [_P, _u64, _P, _u64]
+    L.uot_convergence_error.restype = _d
+    L.uot_rank_partition.argtypes = [_u64, _u64, _P]
+    L.uot_gen_problem_f32.argtypes = [_u64, _u64, _u64, _P, _P, _P, _i]
+    _lib = L
+    return L
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+def _raise(code: int, what: str):
+    raise _ERRORS.get(code, Error)(what)
+
+
+# ------------------------------------------------------------------ types --
+
+
+@dataclass
+class Problem:
+    """Problem<float> (problem.hpp:19-28): a (M x N), rpd (M), cpd (N), er, ep."""
+    a: np.ndarray
+    rpd: np.ndarray
+    cpd: np.ndarray
+    er: float = 1.0
+    ep: float = 1.0
+
+    def m(self) -> int:
+        return int(self.a.shape[0])
+
+    def n(self) -> int:
+        return int(self.a.shape[1])
+
+
+@dataclass
+class ScalingFactors:
+    alpha: np.ndarray = field(default_factory=lambda: np.empty(0))
+    beta: np.ndarray = field(default_factory=lambda: np.empty(0))
+
+
+@dataclass
+class SolveReport:
+    solver: str = ""
+    iterations: int = 0
+    final_error: float = 0.0
+    converged: bool = False
+    wall_ms: float = 0.0
+
+
+@dataclass
+class SolveResult:
+    plan: np.ndarray
+    factors: ScalingFactors
+    report: SolveReport
+
+
+@dataclass
+class FusedState:
+    col_sums: np.ndarray
+
+
+@dataclass
+class RankPartition:
+    ranks: int
+    blocks: list  # [(begin, end)]
+
+    @staticmethod
+    def make(ranks: int, rows: int) -> "RankPartition":
+        b = np.zeros(max(int(ranks), 0) + 1, np.uint64)
+        rc = lib().uot_rank_partition(int(ranks), int(rows), _ptr(b))
+        if rc:
+            _raise(rc, f"RankPartition: {ranks} ranks for {rows} rows would leave a rank without rows")
+        return RankPartition(int(ranks), [(int(b[r]), int(b[r + 1])) for r in range(int(ranks))])
+
+
+# ----------------------------------------------------------------- scalars --
+
+
+def compute_fi(er: float, ep: float) -> float:
+    out = _d()
+    if lib().uot_compute_fi(float(er), float(ep), C.byref(out)):
+        _raise(1, "compute_fi: er must be positive and finite, ep non-negative and finite")
+    return out.value
+
+
+def rescale_factor(target: float, s: float, fi: float) -> float:
+    out = _d()
+    if lib().uot_rescale_factor(float(target), float(s), float(fi), C.byref(out)):
+        _raise(2, "rescale_factor: slice sum is not strictly positive or factor left the positive finite range")
+    return out.value
+
+
+def convergence_error(f: ScalingFactors) -> float:
+    a = np.ascontiguousarray(f.alpha, np.float64)
+    b = np.ascontiguousarray(f.beta, np.float64)
+    return lib().uot_convergence_error(_ptr(a), a.size, _ptr(b), b.size)
+
+
+def gen_problem_t(seed: int, m: int, n: int, threads: int = 0) -> Problem:
+    """gen_problem_t<float> (problem_io.hpp:17-31); er = ep = 1."""
+    if m < 1 or n < 1:
+        _raise(1, "gen_problem: matrix must be at least 1x1")
+    a = np.empty((m, n), np.float32)
+    rpd = np.empty(m, np.float64)
+    cpd = np.empty(n, np.float64)
+    lib().uot_gen_problem_f32(int(seed), m, n, _ptr(a), _ptr(rpd), _ptr(cpd),
+                              threads or (os.cpu_count() or 1))
+    return Problem(a, rpd, cpd, 1.0, 1.0)
+
+
+# ---------------------------------------------------------------- session --
+
+
+class Session:
+    """A problem resident in HBM on one GPU (or one rank's row block of it).
+
+    The device-resident form of fused_solve's loop (fused.hpp:259-285):
+    set_problem -> init_col_sums -> iterate(k, tol) -> factors()/plan().
+    """
+
+    def __init__(self, rows: int, cols: int, device: int = 0, *, dist=None):
+        self._h = _P()
+        L = lib()
+        if dist is None:
+            rc = L.uot_create(C.byref(self._h), int(rows), int(cols), UOT_F32, int(device))
+        else:
+            rank, nranks, nccl_id = dist
+            idbuf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id).ljust(128, b"\0"))
+            rc = L.uot_create_dist(C.byref(self._h), int(rows), int(cols), UOT_F32, int(device),
+                                   int(rank), int(nranks), C.cast(idbuf, _P))
+        if rc:
+            msg = self._err()
+            self.close()
+            _raise(rc, msg)
+        lay = Layout()
+        L.uot_get_layout(self._h, C.byref(lay))
+        self.layout = lay.as_dict()
+        self.rows = int(lay.rows)
+        self.cols = int(lay.cols)
+        self.row_offset = int(lay.row_offset)
+
+    # -- plumbing
+    def _err(self) -> str:
+        return lib().uot_last_error(self._h).decode() if self._h else "session creation failed"
+
+    def _check(self, rc: int):
+        if rc:
+            _raise(rc, self._err())
+
+    def close(self):
+        if self._h:
+            lib().uot_destroy(self._h)
+            self._h = _P()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(lib().uot_get_stream(self._h) or 0)
+
+    # -- problem
+    def set_problem(self, p: Problem):
+        a = np.ascontiguousarray(p.a, np.float32)
+        if a.shape != (self.rows, self.cols):
+            _raise(1, f"matrix shape {a.shape} does not match the session ({self.rows}, {self.cols})")
+        rpd = np.ascontiguousarray(p.rpd, np.float64)
+        cpd = np.ascontiguousarray(p.cpd, np.float64)
+        if rpd.size != self.rows:
+            _raise(1, f"row-marginal length {rpd.size} does not match row count {self.rows}")
+        if cpd.size != self.cols:
+            _raise(1, f"column-marginal length {cpd.size} does not match column count {self.cols}")
+        self._check(lib().uot_set_problem(self._h, _ptr(a), _ptr(rpd), _ptr(cpd), float(p.er), float(p.ep)))
+
+    def set_fi(self, fi: float):
+        self._check(lib().uot_set_fi(self._h, float(fi)))
+
+    def generate_problem(self, seed: int, er: float = 1.0, ep: float = 1.0):
+        self._check(lib().uot_generate_problem(self._h, int(seed), float(er), float(ep)))
+
+    def set_plan(self, a: np.ndarray):
+        a = np.ascontiguousarray(a, np.float32)
+        if a.shape != (self.rows, self.cols):
+            _raise(1, "fused_iterate: matrix shape does not match problem")
+        self._check(lib().uot_set_plan(self._h, _ptr(a)))
+
+    # -- the path
+    def init_col_sums(self):
+        self._check(lib().uot_init_col_sums(self._h))
+
+    def set_col_sums(self, cs: np.ndarray):
+        cs = np.ascontiguousarray(cs, np.float64)
+        if cs.size != self.cols:
+            _raise(1, "fused_iterate: carried column sums have wrong length")
+        self._check(lib().uot_set_col_sums(self._h, _ptr(cs)))
+
+    def col_sums(self) -> np.ndarray:
+        out = np.empty(self.cols, np.float64)
+        self._check(lib().uot_get_col_sums(self._h, _ptr(out)))
+        return out
+
+    def iterate(self, k: int = 1, tol: float = 1e-300):
+        """Up to k iterations; returns (iterations, final_error, converged)."""
+        it, err, conv = _u64(), _d(), _i()
+        self._check(lib().uot_iterate(self._h, int(k), float(tol), C.byref(it), C.byref(err), C.byref(conv)))
+        return int(it.value), float(err.value), bool(conv.value)
+
+    def factors(self) -> ScalingFactors:
+        alpha = np.empty(self.rows, np.float64)
+        beta = np.empty(self.cols, np.float64)
+        self._check(lib().uot_get_factors(self._h, _ptr(alpha), _ptr(beta)))
+        return ScalingFactors(alpha, beta)
+
+    def plan(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.rows, self.cols), np.float32)
+        self._check(lib().uot_get_plan(self._h, _ptr(out)))
+        return out
+
+    def report(self):
+        it, err, conv = _u64(), _d(), _i()
+        self._check(lib().uot_get_report(self._h, C.byref(it), C.byref(err), C.byref(conv)))
+        return int(it.value), float(err.value), bool(conv.value)
+
+    def comm_stats(self):
+        calls, dbl = _u64(), _u64()
+        self._check(lib().uot_get_comm_stats(self._h, C.byref(calls), C.byref(dbl)))
+        return int(calls.value), int(dbl.value)
+
+    def set_timing(self, on: bool = True):
+        self._check(lib().uot_set_timing(self._h, 1 if on else 0))
+
+    def timing(self):
+        s, f, n = _d(), _d(), _u64()
+        self._check(lib().uot_get_timing(self._h, C.byref(s), C.byref(f), C.byref(n)))
+        return float(s.value), float(f.value), int(n.value)
+
+    def kernel_launches(self) -> int:
+        return int(lib().uot_kernel_launches(self._h))
+
+
+# ------------------------------------------------------------- solver API --
+
+
+def _validate_controls(tol: float, max_iter: int, who: str):
+    if not (tol > 0.0):
+        _raise(1, f"{who}: tol must be positive")
+    if max_iter < 1:
+        _raise(1, f"{who}: max_iter must be at least 1")
+
+
+def fused_solve(p: Problem, tol: float, max_iter: int, device: int = 0,
+                session: Session | None = None) -> SolveResult:
+    """fused_solve (fused.hpp:259-285) on one B200.
+
+    report.wall_ms covers upload, seed, iterations and download (the reference's
+    covers seed + iterations of an in-memory matrix)."""
+    _validate_controls(tol, max_iter, "fused_solve")
+    t0 = time.perf_counter()
+    own = session is None
+    s = Session(p.m(), p.n(), device) if own else session
+    try:
+        s.set_problem(p)
+        s.init_col_sums()
+        it, err, conv = s.iterate(max_iter, tol)
+        f = s.factors()
+        plan = s.plan()
+    finally:
+        if own:
+            s.close()
+    rep = SolveReport("cuda", it, err, conv, (time.perf_counter() - t0) * 1e3)
+    return SolveResult(plan, f, rep)
+
+
+def init_col_sums(a: np.ndarray, device: int = 0) -> np.ndarray:
+    """init_col_sums (fused.hpp:71-110) of a host matrix, computed on the GPU."""
+    a = np.ascontiguousarray(a, np.float32)
+    m, n = a.shape
+    with Session(m, n, device) as s:
+        s.set_problem(Problem(a, np.ones(m), np.ones(n), 1.0, 1.0))
+        s.init_col_sums()
+        return s.col_sums()
+
+
+def fused_iterate(a: np.ndarray, state: FusedState, p: Problem, fi: float, device: int = 0,
+                  session: Session | None = None) -> ScalingFactors:
+    """fused_iterate (fused.hpp:164-191) with the reference's host-in/host-out
+    contract: `a` and `state.col_sums` are updated in place. Each call moves the
+    matrix over PCIe; keep a Session for device-resident loops."""
+    if a.shape != (p.m(), p.n()):
+        _raise(1, "fused_iterate: matrix shape does not match problem")
+    if np.asarray(state.col_sums).size != p.n():
+        _raise(1, "fused_iterate: carried column sums have wrong length")
+    own = session is None
+    s = Session(p.m(), p.n(), device) if own else session
+    try:
+        s.set_problem(Problem(a, p.rpd, p.cpd, p.er, p.ep))
+        s.set_fi(fi)  # the caller's exponent, bit for bit
+        s.set_col_sums(state.col_sums)
+        s.iterate(1, 1e-300)
+        f = s.factors()
+        s.plan(out=a) if a.flags.c_contiguous and a.dtype == np.float32 else a.__setitem__(Ellipsis, s.plan())
+        state.col_sums = s.col_sums()
+    finally:
+        if own:
+            s.close()
+    return f
