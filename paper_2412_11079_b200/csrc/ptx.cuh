@@ -103,6 +103,27 @@ __device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// 128-bit single-copy-atomic global accesses (sm_90+): a value and its tag
+// travel together, so the cross-CTA exchange needs no fences at all.
+__device__ __forceinline__ void st_relaxed_b128(void* p, unsigned long long lo, unsigned long long hi) {
+  asm volatile(
+      "{\n\t.reg .b128 v;\n\tmov.b128 v, {%1, %2};\n\tst.relaxed.gpu.global.b128 [%0], v;\n\t}" ::"l"(p),
+      "l"(lo), "l"(hi)
+      : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_b128(const void* p, unsigned long long& lo, unsigned long long& hi) {
+  asm volatile(
+      "{\n\t.reg .b128 v;\n\tld.relaxed.gpu.global.b128 v, [%2];\n\tmov.b128 {%0, %1}, v;\n\t}"
+      : "=l"(lo), "=l"(hi)
+      : "l"(p)
+      : "memory");
+}
+
+// mbarrier arrive (count 1, release at CTA scope) and a parity wait that backs off.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // ----------------------------------------------- exact f32 <-> f64 (RN) --
 // f32 -> f64 with two integer ops (exponent rebias + mantissa funnel). Exact for
 // positive normal floats, which is every value the sweep stores while the

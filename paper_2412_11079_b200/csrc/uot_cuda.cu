@@ -23,7 +23,7 @@ using namespace uotk;
 
 namespace {
 
-constexpr int kNbuf = 6;            // shared-memory ring slots of the sweep
+constexpr int kNbuf = 7;            // shared-memory ring slots of the sweep
 constexpr unsigned kSliceMax = 8192;  // floats of a row one CTA owns (32 KiB)
 
 // ------------------------------------------------------------ kernel table --
@@ -31,12 +31,13 @@ using SweepFn = void (*)(const SweepArgs);
 struct SweepCfg {
   int nt, v, bm;
   SweepFn iter, iter_x, seed;
+  size_t (*smem_bytes)(unsigned buf_stride);
 };
 
 template <int NT, int V, int BM, bool HAS_X>
 SweepCfg make_cfg() {
   SweepCfg c{NT, V, BM, sweep_kernel<NT, V, BM, kNbuf, false, false>, nullptr,
-             sweep_kernel<NT, V, BM, kNbuf, false, true>};
+             sweep_kernel<NT, V, BM, kNbuf, false, true>, &SweepSmem<NT / 32, BM, kNbuf>::bytes};
   if constexpr (HAS_X) c.iter_x = sweep_kernel<NT, V, BM, kNbuf, true, false>;
   return c;
 }
@@ -44,7 +45,7 @@ SweepCfg make_cfg() {
 const std::vector<SweepCfg>& cfg_table() {
   static const std::vector<SweepCfg> t = {
       make_cfg<128, 1, 4, false>(), make_cfg<256, 1, 8, false>(), make_cfg<512, 1, 4, false>(),
-      make_cfg<512, 2, 2, true>(),  make_cfg<512, 3, 1, true>(),  make_cfg<512, 4, 1, true>(),
+      make_cfg<512, 2, 2, false>(), make_cfg<512, 3, 1, true>(),  make_cfg<512, 4, 1, true>(),
   };
   return t;
 }
@@ -115,8 +116,8 @@ struct uot_ctx {
   // device buffers
   float* P = nullptr;
   double *rpd = nullptr, *cpd = nullptr, *alpha = nullptr, *beta2 = nullptr, *col_sums = nullptr,
-         *xsum = nullptr, *partials = nullptr, *cta_err = nullptr, *xval = nullptr;
-  unsigned long long* xflag = nullptr;
+         *xsum = nullptr, *partials = nullptr, *cta_err = nullptr;
+  ulonglong2* xrec = nullptr;
   Control* ctl = nullptr;
   int* dflag = nullptr;
   Control* h_ctl = nullptr;  // pinned mirror
@@ -178,9 +179,7 @@ int plan_layout(uot_ctx* ctx) {
   ctx->groups = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->rows, ctx->sms / G)));
   ctx->grid = ctx->groups * G;
   ctx->buf_stride = round_up(ctx->B * slice * 4u, 128);
-  const int nw = cfg->nt / 32;
-  ctx->smem = static_cast<size_t>(kNbuf) * ctx->buf_stride + kNbuf * 8 +
-              (2 * nw * cfg->bm + 2 * cfg->bm + nw) * sizeof(double);
+  ctx->smem = cfg->smem_bytes(ctx->buf_stride);
   ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * 4 > (64ull << 20) ? 1 : 0;
   for (SweepFn fn : {cfg->iter, cfg->iter_x, cfg->seed}) {
     if (!fn) continue;
@@ -211,13 +210,12 @@ int alloc_all(uot_ctx* ctx) {
   if ((rc = dalloc(ctx, &ctx->xsum, pitch + ctx->nranks))) return rc;
   if ((rc = dalloc(ctx, &ctx->partials, static_cast<size_t>(ctx->groups) * pitch))) return rc;
   if ((rc = dalloc(ctx, &ctx->cta_err, ctx->grid))) return rc;
-  const size_t xn = static_cast<size_t>(ctx->grid) * kRing * ctx->cfg->bm;
-  if ((rc = dalloc(ctx, &ctx->xval, xn))) return rc;
-  if ((rc = dalloc(ctx, &ctx->xflag, xn))) return rc;
+  const size_t xn = static_cast<size_t>(ctx->grid) * kRing;
+  if ((rc = dalloc(ctx, &ctx->xrec, xn))) return rc;
   if ((rc = dalloc(ctx, &ctx->ctl, 1))) return rc;
   if ((rc = dalloc(ctx, &ctx->dflag, 1))) return rc;
   if ((rc = ctx->cuda(cudaMallocHost(&ctx->h_ctl, sizeof(Control)), "cudaMallocHost"))) return rc;
-  CK(cudaMemsetAsync(ctx->xflag, 0, xn * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->xrec, 0, xn * sizeof(ulonglong2), ctx->stream));
   CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), ctx->stream));
   CK(cudaMemsetAsync(ctx->beta2, 0, 2 * pitch * sizeof(double), ctx->stream));
   CK(cudaMemsetAsync(ctx->cpd, 0, pitch * sizeof(double), ctx->stream));
@@ -246,8 +244,7 @@ SweepArgs sweep_args(const uot_ctx* ctx) {
   a.alpha = ctx->alpha;
   a.partials = ctx->partials;
   a.cta_err = ctx->cta_err;
-  a.xval = ctx->xval;
-  a.xflag = ctx->xflag;
+  a.xrec = ctx->xrec;
   a.ctl = ctx->ctl;
   a.rows = ctx->rows;
   a.pitch = ctx->pitch;
@@ -286,7 +283,7 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
   SweepFn fn = seed ? ctx->cfg->seed : (xchg ? ctx->cfg->iter_x : ctx->cfg->iter);
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctx->grid);
-  lc.blockDim = dim3(ctx->cfg->nt);
+  lc.blockDim = dim3(ctx->cfg->nt + 32);  // compute warps + the control warp
   lc.dynamicSmemBytes = ctx->smem;
   lc.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
@@ -467,7 +464,7 @@ void uot_destroy(uot_ctx* ctx) {
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
   for (auto e : ctx->ev) cudaEventDestroy(e);
   void* bufs[] = {ctx->P,     ctx->rpd,   ctx->cpd,      ctx->alpha,   ctx->beta2, ctx->col_sums, ctx->xsum,
-                  ctx->partials, ctx->cta_err, ctx->xval, ctx->xflag, ctx->ctl, ctx->dflag};
+                  ctx->partials, ctx->cta_err, ctx->xrec, ctx->ctl, ctx->dflag};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -488,7 +485,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->G = ctx->G;
   o->groups = ctx->groups;
   o->rows_per_step = ctx->B;
-  o->threads = ctx->cfg->nt;
+  o->threads = ctx->cfg->nt + 32;
   o->chunks = ctx->cfg->v;
   o->smem_bytes = static_cast<uint32_t>(ctx->smem);
   o->nbuf = kNbuf;
