@@ -13,6 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libuot_cuda.so")
+TRACE_SO = os.path.join(PKG, "libuot_cuda_trace.so")  # phase-timer build for profiling runs
 SOURCES = [os.path.join(CSRC, "uot_cuda.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")] + [
     os.path.join(ROOT, "include", "uot_cuda.h")]
@@ -51,5 +52,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return SO
 
 
+def build_trace() -> str:
+    cmd = nvcc_cmd(TRACE_SO, ["-DUOT_TRACE"])
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building the trace build")
+    return TRACE_SO
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    if "--trace" in sys.argv:
+        build_trace()
+    build(force="--force" in sys.argv, verbose="--quiet" not in sys.argv)

@@ -20,7 +20,7 @@ namespace uotk {
 
 struct FinalizeArgs {
   const double* partials;  // [groups][pitch]
-  const double* cta_err;   // [grid]
+  const double* cta_err;   // [grid][2]
   const double* cpd;       // [cols]
   double* beta2;           // [2][pitch]
   double* col_sums;        // [cols]  carried FusedState::col_sums
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs f) {
     if (j < f.nranks) {  // this rank's alpha error in its own slot, zeros elsewhere
       double e = 0.0;
       if (j == f.rank && MODE == kFinIter)
-        for (unsigned c = 0; c < f.grid; ++c) e = fmax(e, f.cta_err[c]);
+        for (unsigned c = 0; c < 2 * f.grid; ++c) e = fmax(e, f.cta_err[c]);
       f.xsum[f.cols + j] = e;
     }
     return;
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const FinalizeArgs f) {
         const unsigned long long t = it + 1;
         double ea = 0.0;
         if (REDUCE) {
-          for (unsigned c = 0; c < f.grid; ++c) ea = fmax(ea, f.cta_err[c]);
+          for (unsigned c = 0; c < 2 * f.grid; ++c) ea = fmax(ea, f.cta_err[c]);
         } else {
           for (unsigned r = 0; r < f.nranks; ++r) ea = fmax(ea, f.xsum[f.cols + r]);
         }

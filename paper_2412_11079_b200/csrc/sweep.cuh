@@ -50,7 +50,7 @@ struct SweepArgs {
   const double* rpd;          // [rows] row marginals
   double* alpha;              // [rows] row factors (output)
   double* partials;           // [groups][pitch] column partials (output)
-  double* cta_err;            // [grid] max|alpha-1| seen by each CTA (output)
+  double* cta_err;            // [grid][2] max|alpha-1| seen by each CTA's factor warps (output)
   ulonglong2* xrec;           // [grid][kRing] exchanged {partial bits, tag} (G > 1)
   Control* ctl;
   unsigned long long rows;    // local rows
@@ -64,34 +64,179 @@ struct SweepArgs {
   double fi;
 };
 
+// Optional phase timers (build with -DUOT_TRACE): clock64 cycles per phase,
+// summed over CTAs into uot_trace[]; read back with uot_trace_read().
+#ifdef UOT_TRACE
+__device__ unsigned long long uot_trace[32];
+#define TR_DECL unsigned long long tr_t0 = 0, tr_acc[32] = {0}; (void)tr_t0;
+#define TR_BEGIN() tr_t0 = clock64()
+#define TR_END(id) tr_acc[id] += clock64() - tr_t0
+#define TR_FLUSH(lo, hi)                                                   \
+  for (int i_ = lo; i_ < hi; ++i_) atomicAdd(&uot_trace[i_], tr_acc[i_])
+#else
+#define TR_DECL
+#define TR_BEGIN()
+#define TR_END(id)
+#define TR_FLUSH(lo, hi)
+#endif
+
 constexpr int kRing = 8;   // exchange records per CTA
 constexpr int kQ = 4;      // ring depth of row partials / factors handed between roles
-
-struct D4 {
-  double a, b, c, d;
-};
-
-// Exact hardware conversion, out of line so the fast path stays branch-only.
-__device__ __noinline__ D4 cvt4_slow(float4 v) { return D4{v.x, v.y, v.z, v.w}; }
-
-// f64 of four stored fp32 values. Fast path: all four positive normal
-// (exponent rebias + mantissa shift, two integer ops each).
-__device__ __forceinline__ D4 cvt4(float4 v) {
-  const uint32_t u0 = __float_as_uint(v.x), u1 = __float_as_uint(v.y);
-  const uint32_t u2 = __float_as_uint(v.z), u3 = __float_as_uint(v.w);
-  const uint32_t m = max(max(max(u0 - 0x800000u, u1 - 0x800000u), u2 - 0x800000u), u3 - 0x800000u);
-  D4 o{__hiloint2double(static_cast<int>((u0 >> 3) + 0x38000000u), static_cast<int>(u0 << 29)),
-       __hiloint2double(static_cast<int>((u1 >> 3) + 0x38000000u), static_cast<int>(u1 << 29)),
-       __hiloint2double(static_cast<int>((u2 >> 3) + 0x38000000u), static_cast<int>(u2 << 29)),
-       __hiloint2double(static_cast<int>((u3 >> 3) + 0x38000000u), static_cast<int>(u3 << 29))};
-  if (__builtin_expect(m >= 0x7f000000u, 0)) o = cvt4_slow(v);
-  return o;
-}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;  // xor tree: every lane holds the bit-identical total (fp add commutes)
+}
+
+
+// ------------------------------------------------------ per-row sweep bodies --
+// A thread owns float4 chunks q = tid + k*NT (k < V) of the slice. FULL: every
+// chunk exists (slice == 4*NT*V); otherwise missing chunks carry 1.0f through
+// the arithmetic and are never stored or summed.
+//
+// Exactness: f32 -> f64 is two integer ops (fastd) for positive normal floats.
+// Each group of values is screened with one VIADDMNMX per value (nn_max) and
+// routed to hardware conversions if anything is zero/subnormal/inf/nan, so the
+// result equals the reference's double(x) for every input.
+
+__device__ __forceinline__ uint32_t nn_max(uint32_t m, float x) {
+  return max(m, __float_as_uint(x) - 0x800000u);  // >= 0x7f000000 <=> not positive normal
+}
+__device__ __forceinline__ bool nn_ok(uint32_t m) { return m < 0x7f000000u; }
+__device__ __forceinline__ double fastd(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __hiloint2double(static_cast<int>((u >> 3) + 0x38000000u), static_cast<int>(u << 29));
+}
+__device__ __forceinline__ float& comp(float4& v, int e) {
+  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+}
+
+// fused.hpp:125-131 for this thread's part of one row: x <- f32(f64(x)*beta_j),
+// returns the f64 sum of the stored values; `x1bad` when a stored value is not
+// positive normal (sweep 2 then converts this row exactly).
+template <int NT, int V, bool FULL>
+__device__ __forceinline__ double row_sweep1(float4* row, unsigned tid, unsigned nq, const double* beta,
+                                             bool& x1bad) {
+  float4 v[V];
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    v[k] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[k], e));
+  }
+  if (nn_ok(m)) {
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) comp(v[k], e) = d2f(fastd(comp(v[k], e)) * beta[4 * k + e]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        comp(v[k], e) = d2f(static_cast<double>(comp(v[k], e)) * beta[4 * k + e]);
+  }
+  uint32_t m1 = 0;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    if (FULL || q < nq) {
+      row[q] = v[k];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        m1 = nn_max(m1, comp(v[k], e));
+        s[e] += fastd(comp(v[k], e));
+      }
+    }
+  }
+  if (!nn_ok(m1)) {
+    x1bad = true;
+    s[0] = s[1] = s[2] = s[3] = 0.0;
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (FULL || tid + k * NT < nq)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[e] += static_cast<double>(comp(v[k], e));
+  }
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+// fused.hpp:135-142 for this thread's part of one row: x <- f32(f64(x)*alpha),
+// next_j += f64(x).
+template <int NT, int V, bool FULL>
+__device__ __forceinline__ void row_sweep2(float4* row, unsigned tid, unsigned nq, double al, bool x1bad,
+                                           double* acc) {
+  float4 v[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    v[k] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
+  }
+  if (!x1bad) {
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) comp(v[k], e) = d2f(fastd(comp(v[k], e)) * al);
+  } else {
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) comp(v[k], e) = d2f(static_cast<double>(comp(v[k], e)) * al);
+  }
+  uint32_t m2 = 0;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    if (FULL || q < nq) {
+      row[q] = v[k];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) m2 = nn_max(m2, comp(v[k], e));
+    }
+  }
+  if (nn_ok(m2)) {
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (FULL || tid + k * NT < nq)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * k + e] += fastd(comp(v[k], e));
+  } else {
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (FULL || tid + k * NT < nq)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * k + e] += static_cast<double>(comp(v[k], e));
+  }
+}
+
+// fused.hpp:96-110 seed: next_j += f64(x) over the stored values.
+template <int NT, int V, bool FULL>
+__device__ __forceinline__ void row_seed(const float4* row, unsigned tid, unsigned nq, double* acc) {
+  float4 v[V];
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    v[k] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[k], e));
+  }
+  if (nn_ok(m)) {
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (FULL || tid + k * NT < nq)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * k + e] += fastd(comp(v[k], e));
+  } else {
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (FULL || tid + k * NT < nq)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * k + e] += static_cast<double>(comp(v[k], e));
+  }
 }
 
 // Shared-memory layout shared by host sizing and the kernel.
@@ -104,19 +249,18 @@ struct SweepSmem {
   }
 };
 
-// NT compute threads (+32 control), V float4 chunks per thread per row
-// (slice <= 4*NT*V), BM max rows per batch, NBUF ring slots, XCHG: G > 1
-// (cross-CTA row-sum exchange), SEED: the read-only init_col_sums sweep.
-template <int NT, int V, int BM, int NBUF, bool XCHG, bool SEED>
-__global__ void __launch_bounds__(NT + 32, 1) sweep_kernel(const SweepArgs a) {
+// NT compute threads + a producer warp + NF factor warps. V float4 chunks per
+// thread per row (slice <= 4*NT*V; FULL: equality), BM max rows per batch, NBUF
+// ring slots. LA: batches between sweep 1 and sweep 2 of a batch beyond the
+// next one (the factor warps' latency budget). XCHG: G > 1, row sums are
+// exchanged across the group. SEED: the read-only init_col_sums sweep.
+template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, bool FULL, bool SEED>
+__global__ void __launch_bounds__(NT + 32 * (XCHG ? 3 : 2), 1) sweep_kernel(const SweepArgs a) {
   constexpr int NW = NT / 32;
-  constexpr int LA = XCHG ? 1 : 0;  // extra batches until a row factor is known
-  // ring: L loading + batch in sweep 1 + LA waiting + batch in sweep 2 + one storing
-  constexpr int L = SEED ? NBUF : NBUF - LA - 3;
-  constexpr int STORE_SLACK = NBUF - L - LA - 2;  // stores issued after the slot's last one
-  static_assert(L >= 1 && (SEED || STORE_SLACK >= 0), "ring too small");
+  constexpr int NF = XCHG ? 2 : 1;  // factor warps
+  static_assert(LA >= 1 && LA <= 2 && (!XCHG || LA == 2), "lag");
+  static_assert(NBUF >= LA + 4, "ring too small");
   static_assert(!XCHG || BM == 1, "the exchange path moves one row per batch");
-  using Smem = SweepSmem<NW, BM, NBUF>;
 
   extern __shared__ __align__(128) unsigned char smem[];
   Control* ctl = a.ctl;
@@ -166,9 +310,13 @@ __global__ void __launch_bounds__(NT + 32, 1) sweep_kernel(const SweepArgs a) {
     return reinterpret_cast<float*>(smem + (b % NBUF) * a.buf_stride);
   };
   auto rows_in = [&](unsigned b) -> unsigned { return min(B, nrows - b * B); };
+  TR_DECL
 
   if (warp == NW) {
-    // ======================================================= control warp ==
+    // ===================================================== producer warp ==
+    // Keeps every free ring slot loading; stores a batch as soon as its sweep 2
+    // is done and refills the slot once the bulk engine has read it.
+    if (lane != 0) return;
     const uint64_t pol = a.evict_first ? policy_evict_first() : policy_evict_normal();
     auto issue_load = [&](unsigned b) {
       const unsigned nr = rows_in(b);
@@ -195,69 +343,85 @@ __global__ void __launch_bounds__(NT + 32, 1) sweep_kernel(const SweepArgs a) {
       }
       bulk_commit();
     };
-
-    if (lane == 0)
-      for (unsigned b = 0; b < nb && b < static_cast<unsigned>(L); ++b) issue_load(b);
-
-    if (SEED) {
-      // The compute warps release a slot (done2) as soon as they accumulated it.
-      for (unsigned b = NBUF; b < nb; ++b) {
-        mbar_wait(&done2[(b - NBUF) % NBUF], ((b - NBUF) / NBUF) & 1u);
-        if (lane == 0) issue_load(b);
-        __syncwarp();
+#ifdef UOT_TRACE
+    const unsigned long long tr_p0 = clock64();
+#endif
+    for (unsigned b = 0; b < nb && b < static_cast<unsigned>(NBUF); ++b) issue_load(b);
+    for (unsigned b = 0; b < nb; ++b) {
+      TR_BEGIN();
+      mbar_wait(&done2[b % NBUF], (b / NBUF) & 1u);  // slot b consumed (sweep 2 / seed done)
+      TR_END(4);
+      if (SEED) {
+        if (b + NBUF < nb) issue_load(b + NBUF);
+        continue;
       }
-      return;
+      TR_BEGIN();
+      issue_store(b);
+      TR_END(5);
+      // refill the slot of the previous batch: its store has had a whole batch to drain
+      if (b >= 1 && b - 1 + NBUF < nb) {
+        TR_BEGIN();
+        bulk_wait_read<1>();
+        TR_END(6);
+        TR_BEGIN();
+        issue_load(b - 1 + NBUF);
+        TR_END(7);
+      }
     }
+    if (!SEED) bulk_wait<0>();  // every store landed before the CTA retires
+#ifdef UOT_TRACE
+    tr_acc[8] = clock64() - tr_p0;
+    TR_FLUSH(4, 9);
+#endif
+    return;
+  }
 
+  if (warp > NW) {
+    // ====================================================== factor warps ==
+    // alpha_i = rescale_factor(rpd_i, s_i, fi) (fused.hpp:133) for every row,
+    // ahead of the compute warps' sweep 2. NF warps take batches round robin so
+    // the serial chain of one batch (partials, exchange round trip, pow) may
+    // take NF batch-times.
+    if (SEED) return;
+    const unsigned f = static_cast<unsigned>(warp - NW - 1);
     const unsigned long long tag_hi = static_cast<unsigned long long>(ctl->epoch) << 32;
     double errmax = 0.0;
-    for (unsigned s = 0; s < nb + LA + 2; ++s) {
-      // (a) row factors of batch s (G == 1) or the CTA partial of batch s (G > 1).
-      if (s < nb) {
-        const unsigned nr = rows_in(s);
-        const unsigned q = s % kQ;
-        double rv = 0.0;
-        if (lane < static_cast<int>(nr)) rv = __ldg(&a.rpd[r0 + static_cast<unsigned long long>(s) * B + lane]);
-        mbar_wait(&done1[q], (s / kQ) & 1u);
-        if (lane < static_cast<int>(nr)) {
-          double t = 0.0;
+#ifdef UOT_TRACE
+    const unsigned long long tr_f0 = clock64();
+#endif
+    for (unsigned s = f; s < nb; s += NF) {
+      const unsigned nr = rows_in(s);
+      const unsigned q = s % kQ;
+      double rv = 0.0;
+      if (lane < static_cast<int>(nr)) rv = __ldg(&a.rpd[r0 + static_cast<unsigned long long>(s) * B + lane]);
+      TR_BEGIN();
+      mbar_wait(&done1[q], (s / kQ) & 1u);
+      TR_END(0);
+      TR_BEGIN();
+      double t = 0.0;  // this CTA's partial of row `lane` of the batch, warp order
+      if (lane < static_cast<int>(nr)) {
+        t = red[(q * NW) * BM + lane];
 #pragma unroll
-          for (int w = 0; w < NW; ++w) t += red[(q * NW + w) * BM + lane];  // warp order
-          if (!XCHG) {
-            double al;
-            if (!rescale_factor_dev(rv, t, a.fi, &al)) {
-              atomicOr(&ctl->alpha_bad, 1);
-              al = 1.0;
-            }
-            alpha_s[q * BM + lane] = al;
-            a.alpha[r0 + static_cast<unsigned long long>(s) * B + lane] = al;
-            errmax = fmax(errmax, fabs(al - 1.0));
-          } else {
-            st_relaxed_b128(&a.xrec[static_cast<size_t>(blockIdx.x) * kRing + (s % kRing)],
-                            static_cast<unsigned long long>(__double_as_longlong(t)), tag_hi | (s + 1));
-          }
-        }
-        if (!XCHG) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&alpha_rdy[q]);
-        }
+        for (int w = 1; w < NW; ++w) t += red[(q * NW + w) * BM + lane];
       }
-      // (b) G > 1: gather batch s-1 from the G CTAs of the group (published a
-      //     batch ago), sum in ascending g, derive its factor.
-      if (XCHG && s >= 1 && s - 1 < nb) {
-        const unsigned sp = s - 1;
-        const unsigned q = sp % kQ;
-        double rv = 0.0, v = 0.0;
-        if (lane == 0) rv = __ldg(&a.rpd[r0 + sp]);
+      if (XCHG) {
+        // Publish {partial, tag} for the group, then gather all G partials of
+        // the row and sum them in ascending g (identical bits on every CTA).
+        if (lane == 0)
+          st_relaxed_b128(&a.xrec[static_cast<size_t>(blockIdx.x) * kRing + (s % kRing)],
+                          static_cast<unsigned long long>(__double_as_longlong(t)), tag_hi | (s + 1));
+        TR_END(1);
+        TR_BEGIN();
+        double v = 0.0;
         if (lane < static_cast<int>(G)) {
-          const ulonglong2* rec = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (sp % kRing)];
-          const unsigned long long want = tag_hi | (sp + 1);
+          const ulonglong2* rec = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (s % kRing)];
+          const unsigned long long want = tag_hi | (s + 1);
           unsigned long long lo, hi;
           ld_relaxed_b128(rec, lo, hi);
           if (hi != want) {
             const unsigned long long t0 = globaltimer_ns();
             do {
-              __nanosleep(64);
+              __nanosleep(32);
               ld_relaxed_b128(rec, lo, hi);
               if (hi != want && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
                 atomicOr(&ctl->status, kStatusExchangeTimeout);
@@ -269,38 +433,35 @@ __global__ void __launch_bounds__(NT + 32, 1) sweep_kernel(const SweepArgs a) {
         }
         double tot = 0.0;
         for (unsigned k = 0; k < G; ++k) tot += __shfl_sync(0xffffffffu, v, k);
-        if (lane == 0) {
-          double al;
-          if (!rescale_factor_dev(rv, tot, a.fi, &al)) {
-            atomicOr(&ctl->alpha_bad, 1);
-            al = 1.0;
-          }
-          alpha_s[q * BM] = al;
-          if (g == 0) {
-            a.alpha[r0 + sp] = al;
-            errmax = fmax(errmax, fabs(al - 1.0));
-          }
-          mbar_arrive(&alpha_rdy[q]);
+        t = tot;
+        TR_END(2);
+        TR_BEGIN();
+      }
+      if (lane < static_cast<int>(nr)) {
+        double al;
+        if (!rescale_factor_dev(rv, t, a.fi, &al)) {
+          atomicOr(&ctl->alpha_bad, 1);
+          al = 1.0;
         }
-        __syncwarp();
-      }
-      // (c) store the batch whose sweep 2 finished (compute step s-1), then
-      //     refill the ring: the slot of batch s+L last held batch s+L-NBUF,
-      //     whose store left STORE_SLACK stores ago.
-      if (s >= static_cast<unsigned>(LA + 2) && s - (LA + 2) < nb) {
-        const unsigned b = s - (LA + 2);
-        mbar_wait(&done2[b % NBUF], (b / NBUF) & 1u);
-        if (lane == 0) issue_store(b);
-      }
-      if (s + L < nb && lane == 0) {
-        bulk_wait_read<STORE_SLACK>();
-        issue_load(s + L);
+        alpha_s[q * BM + lane] = al;
+        if (g == 0) {
+          a.alpha[r0 + static_cast<unsigned long long>(s) * B + lane] = al;
+          errmax = fmax(errmax, fabs(al - 1.0));
+        }
       }
       __syncwarp();
+      if (lane == 0) mbar_arrive(&alpha_rdy[q]);
+      TR_END(3);
     }
-    if (lane == 0) bulk_wait<0>();  // every store landed before the CTA retires
     for (int o = 16; o > 0; o >>= 1) errmax = fmax(errmax, __shfl_xor_sync(0xffffffffu, errmax, o));
-    if (lane == 0) a.cta_err[blockIdx.x] = errmax;
+    if (lane == 0) {
+      a.cta_err[2 * blockIdx.x + f] = errmax;
+      if (NF == 1) a.cta_err[2 * blockIdx.x + 1] = 0.0;
+    }
+#ifdef UOT_TRACE
+    tr_acc[9] = clock64() - tr_f0;
+    if (lane == 0 && f == 0) { TR_FLUSH(0, 4); TR_FLUSH(9, 10); }
+#endif
     return;
   }
 
@@ -314,64 +475,75 @@ __global__ void __launch_bounds__(NT + 32, 1) sweep_kernel(const SweepArgs a) {
     for (int k = 0; k < V; ++k) {
       const unsigned q = tid + k * NT;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) beta[4 * k + e] = q < nq ? bsrc[4 * q + e] : 0.0;
+      for (int e = 0; e < 4; ++e) beta[4 * k + e] = (FULL || q < nq) ? bsrc[4 * q + e] : 1.0;
     }
   }
 
+  uint32_t x1bad = 0;  // bit (b % 4) * 8 + r: row r of batch b stored a non-normal x1
+#ifdef UOT_TRACE
+  const unsigned long long tr_c0 = clock64();
+#endif
   const unsigned nsteps = SEED ? nb : nb + LA + 1;
   for (unsigned s = 0; s < nsteps; ++s) {
-    // sweep 1 on batch s (or the seed accumulation).
+    // sweep 1 on batch s (or the seed accumulation); its row partials are
+    // reduced after sweep 2 below so the shuffle latency overlaps that work.
+    double part[BM];
     if (s < nb) {
+      TR_BEGIN();
       mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
+      TR_END(16);
       float* buf = slot_ptr(s);
       const unsigned nr = rows_in(s);
+      TR_BEGIN();
       if (SEED) {
 #pragma unroll
-        for (int r = 0; r < BM; ++r) {
-          if (r < static_cast<int>(nr)) {
-            const float4* row = reinterpret_cast<const float4*>(buf + r * a.slice);
-#pragma unroll
-            for (int k = 0; k < V; ++k) {
-              const unsigned q = tid + k * NT;
-              if (q < nq) {
-                const D4 d = cvt4(row[q]);
-                acc[4 * k + 0] += d.a;
-                acc[4 * k + 1] += d.b;
-                acc[4 * k + 2] += d.c;
-                acc[4 * k + 3] += d.d;
-              }
-            }
-          }
-        }
+        for (int r = 0; r < BM; ++r)
+          if (r < static_cast<int>(nr))
+            row_seed<NT, V, FULL>(reinterpret_cast<const float4*>(buf + r * a.slice), tid, nq, acc);
         __syncwarp();
         if (lane == 0) mbar_arrive(&done2[s % NBUF]);
         continue;
       }
-      double part[BM];
+      const uint32_t shift = (s % 4) * 8;
+      x1bad &= ~(0xffu << shift);
 #pragma unroll
       for (int r = 0; r < BM; ++r) {
         part[r] = 0.0;
         if (r < static_cast<int>(nr)) {
-          float4* row = reinterpret_cast<float4*>(buf + r * a.slice);
-          double sr = 0.0;
-#pragma unroll
-          for (int k = 0; k < V; ++k) {
-            const unsigned q = tid + k * NT;
-            if (q < nq) {
-              float4 v = row[q];
-              const D4 d = cvt4(v);
-              v.x = d2f(d.a * beta[4 * k + 0]);
-              v.y = d2f(d.b * beta[4 * k + 1]);
-              v.z = d2f(d.c * beta[4 * k + 2]);
-              v.w = d2f(d.d * beta[4 * k + 3]);
-              const D4 x1 = cvt4(v);
-              sr = sr + x1.a + x1.b + x1.c + x1.d;
-              row[q] = v;
-            }
-          }
-          part[r] = sr;
+          bool bad = false;
+          part[r] = row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, bad);
+          if (bad) x1bad |= 1u << (shift + r);
         }
       }
+      TR_END(17);
+    }
+
+    // sweep 2 on batch s-1-LA once its factors are published.
+    if (!SEED && s >= static_cast<unsigned>(LA + 1) && s - (LA + 1) < nb) {
+      const unsigned b = s - (LA + 1);
+      const unsigned qb = b % kQ;
+      TR_BEGIN();
+      mbar_wait(&alpha_rdy[qb], (b / kQ) & 1u);
+      TR_END(19);
+      TR_BEGIN();
+      float* buf = slot_ptr(b);
+      const unsigned nr = rows_in(b);
+      const uint32_t shift = (b % 4) * 8;
+#pragma unroll
+      for (int r = 0; r < BM; ++r) {
+        if (r < static_cast<int>(nr))
+          row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq,
+                                  alpha_s[qb * BM + r], (x1bad >> (shift + r)) & 1u, acc);
+      }
+      fence_proxy_async_smem();  // generic writes -> the producer's bulk store
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done2[b % NBUF]);
+      TR_END(20);
+    }
+
+    if (!SEED && s < nb) {
+      TR_BEGIN();
+      const unsigned nr = rows_in(s);
       const unsigned qq = s % kQ;
 #pragma unroll
       for (int r = 0; r < BM; ++r) {
@@ -382,45 +554,13 @@ __global__ void __launch_bounds__(NT + 32, 1) sweep_kernel(const SweepArgs a) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&done1[qq]);
-    }
-
-    // sweep 2 on batch s-1-LA once its factors are published.
-    if (!SEED && s >= static_cast<unsigned>(LA + 1) && s - (LA + 1) < nb) {
-      const unsigned b = s - (LA + 1);
-      const unsigned qb = b % kQ;
-      mbar_wait(&alpha_rdy[qb], (b / kQ) & 1u);
-      float* buf = slot_ptr(b);
-      const unsigned nr = rows_in(b);
-#pragma unroll
-      for (int r = 0; r < BM; ++r) {
-        if (r < static_cast<int>(nr)) {
-          const double al = alpha_s[qb * BM + r];
-          float4* row = reinterpret_cast<float4*>(buf + r * a.slice);
-#pragma unroll
-          for (int k = 0; k < V; ++k) {
-            const unsigned q = tid + k * NT;
-            if (q < nq) {
-              float4 v = row[q];
-              const D4 d = cvt4(v);
-              v.x = d2f(d.a * al);
-              v.y = d2f(d.b * al);
-              v.z = d2f(d.c * al);
-              v.w = d2f(d.d * al);
-              const D4 x2 = cvt4(v);
-              acc[4 * k + 0] += x2.a;
-              acc[4 * k + 1] += x2.b;
-              acc[4 * k + 2] += x2.c;
-              acc[4 * k + 3] += x2.d;
-              row[q] = v;
-            }
-          }
-        }
-      }
-      fence_proxy_async_smem();  // generic writes -> the control warp's bulk store
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&done2[b % NBUF]);
+      TR_END(18);
     }
   }
+#ifdef UOT_TRACE
+  tr_acc[21] = clock64() - tr_c0;
+  if (tid == 0) { TR_FLUSH(16, 22); }
+#endif
 
   // Column partials of this CTA: one row of the [groups][pitch] table.
   double* dst = a.partials + static_cast<size_t>(group) * a.pitch + static_cast<size_t>(g) * a.slice;

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -23,31 +24,52 @@ using namespace uotk;
 
 namespace {
 
-constexpr int kNbuf = 7;            // shared-memory ring slots of the sweep
-constexpr unsigned kSliceMax = 8192;  // floats of a row one CTA owns (32 KiB)
+constexpr unsigned kSliceMax = 8192;      // floats of a row one CTA owns when G == 1 (32 KiB)
+constexpr unsigned kSliceMaxXchg = 8192;  // ... when a row spans G > 1 CTAs
 
 // ------------------------------------------------------------ kernel table --
 using SweepFn = void (*)(const SweepArgs);
 struct SweepCfg {
-  int nt, v, bm;
-  SweepFn iter, iter_x, seed;
+  int nt, v, bm, nbuf;
+  bool xchg;           // rows span G > 1 CTAs (cross-CTA row-sum exchange)
+  SweepFn iter[2];     // [FULL]
+  SweepFn seed[2];     // [FULL]
   size_t (*smem_bytes)(unsigned buf_stride);
 };
 
-template <int NT, int V, int BM, bool HAS_X>
+// G == 1: sweep 2 lags sweep 1 by LA=1 extra batch (the factor warp's budget).
+// G > 1: LA=2, the row partials are gathered one batch after publication.
+template <int NT, int V, int BM, int NB, bool XCHG = false>
 SweepCfg make_cfg() {
-  SweepCfg c{NT, V, BM, sweep_kernel<NT, V, BM, kNbuf, false, false>, nullptr,
-             sweep_kernel<NT, V, BM, kNbuf, false, true>, &SweepSmem<NT / 32, BM, kNbuf>::bytes};
-  if constexpr (HAS_X) c.iter_x = sweep_kernel<NT, V, BM, kNbuf, true, false>;
+  constexpr int LA = XCHG ? 2 : 1;
+  SweepCfg c{};
+  c.nt = NT;
+  c.v = V;
+  c.bm = BM;
+  c.nbuf = NB;
+  c.xchg = XCHG;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, false, false>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, true, false>;
+  c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, false, true>;
+  c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, true, true>;
+  c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
   return c;
 }
 
 const std::vector<SweepCfg>& cfg_table() {
   static const std::vector<SweepCfg> t = {
-      make_cfg<128, 1, 4, false>(), make_cfg<256, 1, 8, false>(), make_cfg<512, 1, 4, false>(),
-      make_cfg<512, 2, 2, false>(), make_cfg<512, 3, 1, true>(),  make_cfg<512, 4, 1, true>(),
+      // G == 1 (rows fit one CTA): 32 KiB ring slots
+      make_cfg<128, 1, 4, 7>(), make_cfg<256, 1, 8, 7>(), make_cfg<512, 1, 4, 7>(),
+      make_cfg<512, 2, 2, 7>(), make_cfg<512, 3, 1, 7>(), make_cfg<512, 4, 1, 7>(),
+      // G > 1: 32 KiB slices; two factor warps overlap the exchange round trips
+      make_cfg<512, 3, 1, 7, true>(), make_cfg<512, 4, 1, 7, true>(),
   };
   return t;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
 }
 
 // ------------------------------------------------------------------- NCCL --
@@ -112,6 +134,7 @@ struct uot_ctx {
   size_t smem = 0;
   const SweepCfg* cfg = nullptr;
   int evict_first = 0;
+  int full = 0;
 
   // device buffers
   float* P = nullptr;
@@ -159,14 +182,15 @@ namespace {
 int plan_layout(uot_ctx* ctx) {
   const uint64_t cols = ctx->cols;
   if (cols > (1ull << 26)) return ctx->fail(UOT_CONFIG_ERROR, "cols %llu too large", (unsigned long long)cols);
-  unsigned G = cols <= kSliceMax ? 1u : static_cast<unsigned>((cols + kSliceMax - 1) / kSliceMax);
+  const unsigned xmax = static_cast<unsigned>(env_int("UOT_SLICE_MAX_XCHG", kSliceMaxXchg));
+  unsigned G = cols <= kSliceMax ? 1u : static_cast<unsigned>((cols + xmax - 1) / xmax);
   if (G > static_cast<unsigned>(ctx->sms) || G > 32)
     return ctx->fail(UOT_CONFIG_ERROR, "cols %llu needs %u CTAs per row (max %d)",
                      (unsigned long long)cols, G, std::min(ctx->sms, 32));
   const unsigned slice = round_up(static_cast<unsigned>((cols + G - 1) / G), 4);
   const SweepCfg* cfg = nullptr;
   for (const auto& c : cfg_table())
-    if (static_cast<unsigned>(c.nt * 4 * c.v) >= slice && (G == 1 || c.iter_x)) {
+    if (static_cast<unsigned>(c.nt * 4 * c.v) >= slice && c.xchg == (G > 1)) {
       cfg = &c;
       break;
     }
@@ -175,13 +199,14 @@ int plan_layout(uot_ctx* ctx) {
   ctx->slice = slice;
   ctx->pitch = slice * G;
   ctx->cfg = cfg;
-  ctx->B = std::max(1u, std::min(static_cast<unsigned>(cfg->bm), kSliceMax / slice));
+  ctx->B = G > 1 ? 1u : std::max(1u, std::min(static_cast<unsigned>(cfg->bm), kSliceMax / slice));
   ctx->groups = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->rows, ctx->sms / G)));
   ctx->grid = ctx->groups * G;
   ctx->buf_stride = round_up(ctx->B * slice * 4u, 128);
   ctx->smem = cfg->smem_bytes(ctx->buf_stride);
   ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * 4 > (64ull << 20) ? 1 : 0;
-  for (SweepFn fn : {cfg->iter, cfg->iter_x, cfg->seed}) {
+  ctx->full = slice == static_cast<unsigned>(4 * cfg->nt * cfg->v) ? 1 : 0;
+  for (SweepFn fn : {cfg->iter[ctx->full], cfg->seed[ctx->full]}) {
     if (!fn) continue;
     const int rc = ctx->cuda(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -209,7 +234,7 @@ int alloc_all(uot_ctx* ctx) {
   if ((rc = dalloc(ctx, &ctx->col_sums, pitch))) return rc;
   if ((rc = dalloc(ctx, &ctx->xsum, pitch + ctx->nranks))) return rc;
   if ((rc = dalloc(ctx, &ctx->partials, static_cast<size_t>(ctx->groups) * pitch))) return rc;
-  if ((rc = dalloc(ctx, &ctx->cta_err, ctx->grid))) return rc;
+  if ((rc = dalloc(ctx, &ctx->cta_err, 2 * static_cast<size_t>(ctx->grid)))) return rc;
   const size_t xn = static_cast<size_t>(ctx->grid) * kRing;
   if ((rc = dalloc(ctx, &ctx->xrec, xn))) return rc;
   if ((rc = dalloc(ctx, &ctx->ctl, 1))) return rc;
@@ -280,10 +305,11 @@ FinalizeArgs fin_args(const uot_ctx* ctx) {
 int launch_sweep(uot_ctx* ctx, bool seed) {
   const SweepArgs a = sweep_args(ctx);
   const bool xchg = !seed && ctx->G > 1;
-  SweepFn fn = seed ? ctx->cfg->seed : (xchg ? ctx->cfg->iter_x : ctx->cfg->iter);
+  SweepFn fn = seed ? ctx->cfg->seed[ctx->full] : ctx->cfg->iter[ctx->full];
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctx->grid);
-  lc.blockDim = dim3(ctx->cfg->nt + 32);  // compute warps + the control warp
+  // compute warps + producer warp + factor warp(s)
+  lc.blockDim = dim3(ctx->cfg->nt + (!seed && ctx->cfg->xchg ? 96 : 64));
   lc.dynamicSmemBytes = ctx->smem;
   lc.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
@@ -485,10 +511,10 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->G = ctx->G;
   o->groups = ctx->groups;
   o->rows_per_step = ctx->B;
-  o->threads = ctx->cfg->nt + 32;
+  o->threads = ctx->cfg->nt + (ctx->cfg->xchg ? 96 : 64);
   o->chunks = ctx->cfg->v;
   o->smem_bytes = static_cast<uint32_t>(ctx->smem);
-  o->nbuf = kNbuf;
+  o->nbuf = ctx->cfg->nbuf;
   o->sms = ctx->sms;
   o->rank = ctx->rank;
   o->nranks = ctx->nranks;
@@ -690,6 +716,22 @@ int uot_get_timing(const uot_ctx* ctx, double* sweep_ms, double* finalize_ms, ui
 }
 
 uint64_t uot_kernel_launches(const uot_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// Phase timers of the trace build (-DUOT_TRACE); returns UOT_CONFIG_ERROR otherwise.
+UOT_API int uot_trace_read(unsigned long long* out32, int reset) {
+#ifdef UOT_TRACE
+  if (cudaMemcpyFromSymbol(out32, uot_trace, 32 * sizeof(unsigned long long)) != cudaSuccess) return UOT_CUDA_ERROR;
+  if (reset) {
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(uot_trace, z, sizeof(z));
+  }
+  return UOT_OK;
+#else
+  (void)out32;
+  (void)reset;
+  return UOT_CONFIG_ERROR;
+#endif
+}
 
 // ------------------------------------------------------------ host scalars --
 int uot_compute_fi(double er, double ep, double* fi) {  // scaling.cpp:9-13

@@ -96,7 +96,7 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.SO
+    path = os.environ.get("UOT_LIB_PATH") or _build.SO  # UOT_LIB_PATH: e.g. the trace build
     if not os.path.exists(path):
         if os.environ.get("UOT_AUTOBUILD", "1") == "1":
             try:
