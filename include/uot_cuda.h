@@ -125,6 +125,13 @@ UOT_API int uot_get_col_sums(const uot_ctx* ctx, double* out);
 UOT_API int uot_iterate(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations, double* final_error,
                 int* converged);
 
+/* uot_iterate with the device time of the k iterations (CUDA events on the
+ * session stream around all of its launches) in *device_ms. */
+UOT_API int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations,
+                              double* final_error, int* converged, double* device_ms);
+/* Wait for all work queued on the session stream. */
+UOT_API int uot_synchronize(uot_ctx* ctx);
+
 /* ScalingFactors of the last completed iteration (problem.hpp:30-33); alpha is
  * this rank's rows, beta all columns. */
 UOT_API int uot_get_factors(const uot_ctx* ctx, double* alpha, double* beta);
@@ -142,12 +149,20 @@ UOT_API int uot_get_timing(const uot_ctx* ctx, double* sweep_ms, double* finaliz
 /* Number of kernels this session launched so far (all kinds). */
 UOT_API uint64_t uot_kernel_launches(const uot_ctx* ctx);
 
+/* Page-locked host memory (cudaMallocHost) for fast uploads / downloads. */
+UOT_API void* uot_host_alloc(uint64_t bytes);
+UOT_API void uot_host_free(void* p);
+
 /* ---- scalars and plans (host; scaling.cpp:9-29, plan.cpp:11-44) -------- */
 UOT_API int uot_compute_fi(double er, double ep, double* fi);
 UOT_API int uot_rescale_factor(double target, double sum, double fi, double* out);
 UOT_API double uot_convergence_error(const double* alpha, uint64_t m, const double* beta, uint64_t n);
 /* bounds[0..ranks]: rank r owns [bounds[r], bounds[r+1]). */
 UOT_API int uot_rank_partition(uint64_t ranks, uint64_t rows, uint64_t* bounds);
+/* Rows [row0, row0+rows) of gen_problem_t<float>(seed, global_rows, n): the
+ * block's A, its rpd slice and the full cpd (either may be NULL). */
+UOT_API int uot_gen_block_f32(uint64_t seed, uint64_t global_rows, uint64_t n, uint64_t row0,
+                              uint64_t rows, float* a, double* rpd, double* cpd, int threads);
 /* gen_problem_t<float> on the host (threads > 1 fills A in parallel). */
 UOT_API int uot_gen_problem_f32(uint64_t seed, uint64_t m, uint64_t n, float* a, double* rpd, double* cpd,
                         int threads);

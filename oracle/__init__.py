@@ -73,6 +73,10 @@ class Oracle:
             build()
         self.lib = C.CDLL(LIB)
         L = self.lib
+        L.orc_splitmix64_next.argtypes = [C.POINTER(_u64)]
+        L.orc_splitmix64_next.restype = _u64
+        L.orc_next_unit.argtypes = [C.POINTER(_u64)]
+        L.orc_next_unit.restype = _d
         L.orc_gen_problem_f32.argtypes = [_u64, _sz, _sz, _P, _P, _P, _i]
         L.orc_gen_problem_f64.argtypes = [_u64, _sz, _sz, _P, _P, _P, _i]
         L.orc_compute_fi.argtypes = [_d, _d, C.POINTER(_d)]

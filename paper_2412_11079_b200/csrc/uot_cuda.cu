@@ -127,6 +127,7 @@ struct uot_ctx {
   int sms = 0;
   uint64_t rows = 0, cols = 0, row_offset = 0, global_rows = 0;
   int rank = 0, nranks = 1;
+  bool is_dist = false;  // created by uot_create_dist (CommStats are kept)
   ncclComm_t comm = nullptr;
 
   // layout
@@ -469,6 +470,7 @@ int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtyp
   ctx->cols = cols;
   ctx->rank = rank;
   ctx->nranks = nranks;
+  ctx->is_dist = true;
   int rc = create_common(ctx, device);
   if (rc) return rc;
   if (nranks > 1) {
@@ -622,6 +624,18 @@ int uot_get_col_sums(const uot_ctx* cctx, double* out) {
 
 int uot_iterate(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations, double* final_error,
                 int* converged) {
+  return uot_iterate_timed(ctx, k, tol, iterations, final_error, converged, nullptr);
+}
+
+int uot_synchronize(uot_ctx* ctx) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return UOT_OK;
+}
+
+int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations, double* final_error,
+                      int* converged, double* device_ms) {
   if (!ctx) return UOT_INVALID_PARAMETER;
   if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
   if (!ctx->seeded)
@@ -630,6 +644,12 @@ int uot_iterate(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations, doub
   if (k < 1) return ctx->fail(UOT_INVALID_PARAMETER, "max_iter must be at least 1");
   CK(cudaSetDevice(ctx->device));
   const uint64_t before = ctx->h_ctl->iter;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (device_ms) {
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    CK(cudaEventRecord(t0, ctx->stream));
+  }
   begin_iterate_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctl, tol);
   ctx->launches++;
   CK(cudaGetLastError());
@@ -641,7 +661,15 @@ int uot_iterate(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations, doub
     if ((rc = launch_finalize<kFinIter>(ctx))) return rc;
     if (ctx->timing) record(ctx, 3 * i + 2);
   }
+  if (device_ms) CK(cudaEventRecord(t1, ctx->stream));
   if ((rc = sync_ctl(ctx))) return rc;
+  if (device_ms) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t0, t1));
+    *device_ms = ms;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
   if (ctx->timing) {
     ctx->sweep_ms = ctx->fin_ms = 0.0;
     for (uint64_t i = 0; i < k; ++i) {
@@ -695,7 +723,7 @@ int uot_get_report(const uot_ctx* ctx, uint64_t* iterations, double* final_error
 int uot_get_comm_stats(const uot_ctx* ctx, uint64_t* calls, uint64_t* doubles) {
   if (!ctx || !ctx->h_ctl) return UOT_INVALID_PARAMETER;
   // One allreduce of the column vector per completed iteration (distributed.hpp:88-94).
-  const uint64_t it = ctx->nranks > 1 ? ctx->h_ctl->iter : 0;
+  const uint64_t it = ctx->is_dist ? ctx->h_ctl->iter : 0;
   if (calls) *calls = it;
   if (doubles) *doubles = it * ctx->cols;
   return UOT_OK;
@@ -733,6 +761,15 @@ UOT_API int uot_trace_read(unsigned long long* out32, int reset) {
 #endif
 }
 
+// Pinned host staging for callers that feed the session from host memory.
+void* uot_host_alloc(uint64_t bytes) {
+  void* p = nullptr;
+  return cudaMallocHost(&p, std::max<uint64_t>(bytes, 1)) == cudaSuccess ? p : nullptr;
+}
+void uot_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 // ------------------------------------------------------------ host scalars --
 int uot_compute_fi(double er, double ep, double* fi) {  // scaling.cpp:9-13
   if (!(er > 0.0) || !std::isfinite(er)) return UOT_INVALID_PARAMETER;
@@ -762,9 +799,9 @@ int uot_rank_partition(uint64_t ranks, uint64_t rows, uint64_t* bounds) {  // pl
   return UOT_OK;
 }
 
-int uot_gen_problem_f32(uint64_t seed, uint64_t m, uint64_t n, float* a, double* rpd, double* cpd,
-                        int threads) {  // problem_io.hpp:17-31
-  if (m < 1 || n < 1) return UOT_INVALID_PARAMETER;
+int uot_gen_block_f32(uint64_t seed, uint64_t global_rows, uint64_t n, uint64_t row0, uint64_t rows,
+                      float* a, double* rpd, double* cpd, int threads) {  // problem_io.hpp:17-31
+  if (global_rows < 1 || n < 1 || row0 + rows > global_rows) return UOT_INVALID_PARAMETER;
   auto unit_at = [seed](uint64_t k) {
     uint64_t z = seed + (k + 1) * 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -772,17 +809,24 @@ int uot_gen_problem_f32(uint64_t seed, uint64_t m, uint64_t n, float* a, double*
     z ^= z >> 31;
     return static_cast<double>((z >> 11) + 1) * 0x1p-53;
   };
-  const uint64_t mn = m * n;
+  const uint64_t mn = rows * n, first = row0 * n, gmn = global_rows * n;
   const int nt = std::max(1, std::min<int>(threads, 256));
   std::vector<std::thread> th;
   for (int t = 0; t < nt; ++t)
     th.emplace_back([&, t] {
-      for (uint64_t k = mn * t / nt; k < mn * (t + 1) / nt; ++k) a[k] = static_cast<float>(unit_at(k));
+      for (uint64_t k = mn * t / nt; k < mn * (t + 1) / nt; ++k) a[k] = static_cast<float>(unit_at(first + k));
     });
   for (auto& x : th) x.join();
-  for (uint64_t i = 0; i < m; ++i) rpd[i] = unit_at(mn + i);
-  for (uint64_t j = 0; j < n; ++j) cpd[j] = unit_at(mn + m + j);
+  if (rpd)
+    for (uint64_t i = 0; i < rows; ++i) rpd[i] = unit_at(gmn + row0 + i);
+  if (cpd)
+    for (uint64_t j = 0; j < n; ++j) cpd[j] = unit_at(gmn + global_rows + j);
   return UOT_OK;
+}
+
+int uot_gen_problem_f32(uint64_t seed, uint64_t m, uint64_t n, float* a, double* rpd, double* cpd,
+                        int threads) {
+  return uot_gen_block_f32(seed, m, n, 0, m, a, rpd, cpd, threads);
 }
 
 }  // extern "C"

@@ -1,0 +1,140 @@
+"""Multi-GPU row-sharded solve: one process per GPU, one allreduce per iteration.
+
+Mirror of distributed_solve (/root/reference/proj/core/include/uot/distributed.hpp:52-136).
+The reference simulates P ranks in one process; here each rank is a process
+driving its own B200:
+
+* rows are split by RankPartition::make(P, rows) (src/plan.cpp:35-44) — rank r
+  keeps its contiguous row block resident in HBM;
+* every iteration ends with ONE sum-allreduce of a (cols + P)-vector of f64 over
+  NCCL (NVLink/NVSwitch): the rank's column partials (distributed.hpp:88-94) plus
+  one slot per rank carrying its max|alpha-1| so every rank derives the same
+  convergence error (the "scalar max-reduction" the reference comment at
+  distributed.hpp:50-51 anticipates, folded into the same call);
+* every rank then derives the identical beta from the identical reduced vector
+  (distributed.hpp:96-100).
+
+The NCCL communicator lives inside the C++ session (include/uot_cuda.h,
+uot_create_dist); torch.distributed (any backend, gloo is enough) only carries
+the 128-byte NCCL id from rank 0 and the host-side barriers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import uot
+
+
+@dataclass
+class CommStats:
+    """CommStats (distributed.hpp:24-27)."""
+    allreduce_calls: int = 0
+    doubles_reduced: int = 0
+
+
+@dataclass
+class DistributedResult:
+    """DistributedResult<T> (distributed.hpp:34-40) for THIS rank: the plan and
+    alpha of its row block, the (replicated) beta, the report and CommStats."""
+    plan: np.ndarray
+    factors: uot.ScalingFactors
+    report: uot.SolveReport
+    comm: CommStats = field(default_factory=CommStats)
+    row_begin: int = 0
+    row_end: int = 0
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    rc = uot.lib().uot_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if rc:
+        raise uot.CudaError("ncclGetUniqueId failed (libnccl.so.2 missing?)")
+    return bytes(buf)
+
+
+def _torch_dist():
+    import torch.distributed as dist  # plumbing only
+    if not dist.is_available() or not dist.is_initialized():
+        return None
+    return dist
+
+
+def broadcast_bytes(data: bytes | None, src: int = 0) -> bytes:
+    """Broadcast a small byte string over the initialised torch process group."""
+    dist = _torch_dist()
+    if dist is None:
+        assert data is not None
+        return data
+    obj = [data]
+    dist.broadcast_object_list(obj, src=src)
+    return obj[0]
+
+
+def rank_block(ranks: int, rows: int, rank: int):
+    part = uot.RankPartition.make(ranks, rows)
+    return part.blocks[rank]
+
+
+class DistSession(uot.Session):
+    """Session for rank `rank` of `nranks` over `global_rows` rows. With
+    nranks == 1 it is an ordinary single-GPU session (no NCCL)."""
+
+    def __init__(self, global_rows: int, cols: int, rank: int, nranks: int, device: int,
+                 nccl_id: bytes | None = None):
+        if nranks > 1 and nccl_id is None:
+            raise uot.InvalidParameter("a multi-rank session needs the NCCL id of rank 0")
+        super().__init__(global_rows, cols, device, dist=(rank, nranks, nccl_id or b"\0" * 128))
+        self.rank, self.nranks = rank, nranks
+
+
+def make_session(global_rows: int, cols: int, device: int | None = None) -> DistSession:
+    """Collective: one DistSession per rank of the current torch process group."""
+    dist = _torch_dist()
+    rank = dist.get_rank() if dist else 0
+    world = dist.get_world_size() if dist else 1
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", rank))
+    nid = None
+    if world > 1:
+        nid = broadcast_bytes(nccl_unique_id() if rank == 0 else None, src=0)
+    return DistSession(global_rows, cols, rank, world, device, nid)
+
+
+def distributed_solve(p: uot.Problem, tol: float, max_iter: int, device: int | None = None,
+                      session: DistSession | None = None, global_rows: int | None = None
+                      ) -> DistributedResult:
+    """distributed_solve (distributed.hpp:52-130) across the ranks of the current
+    torch process group (world size 1 without one).
+
+    `p` is the whole problem (every rank slices its RankPartition block), or —
+    with `global_rows` given — already this rank's row block (rpd of the block,
+    cpd of all columns), which avoids materialising the global matrix per host."""
+    uot._validate_controls(tol, max_iter, "distributed_solve")
+    t0 = time.perf_counter()
+    grows = global_rows if global_rows is not None else p.m()
+    own = session is None
+    s = make_session(grows, p.n(), device) if own else session
+    try:
+        b, e = s.row_offset, s.row_offset + s.rows
+        if global_rows is None:
+            local = uot.Problem(p.a[b:e], p.rpd[b:e], p.cpd, p.er, p.ep)
+        else:
+            if p.m() != s.rows:
+                raise uot.PartitionError(f"rank block has {p.m()} rows, partition expects {s.rows}")
+            local = p
+        s.set_problem(local)
+        s.init_col_sums()
+        it, err, conv = s.iterate(max_iter, tol)
+        f = s.factors()
+        plan = s.plan()
+        calls, dbl = s.comm_stats()
+    finally:
+        if own:
+            s.close()
+    rep = uot.SolveReport("dist", it, err, conv, (time.perf_counter() - t0) * 1e3)
+    return DistributedResult(plan, f, rep, CommStats(calls, dbl), b, e)

@@ -124,6 +124,9 @@ def lib():
     L.uot_set_col_sums.argtypes = [_P, _P]
     L.uot_get_col_sums.argtypes = [_P, _P]
     L.uot_iterate.argtypes = [_P, _u64, _d, C.POINTER(_u64), C.POINTER(_d), C.POINTER(_i)]
+    L.uot_iterate_timed.argtypes = [_P, _u64, _d, C.POINTER(_u64), C.POINTER(_d), C.POINTER(_i),
+                                    C.POINTER(_d)]
+    L.uot_synchronize.argtypes = [_P]
     L.uot_get_factors.argtypes = [_P, _P, _P]
     L.uot_get_plan.argtypes = [_P, _P]
     L.uot_get_report.argtypes = [_P, C.POINTER(_u64), C.POINTER(_d), C.POINTER(_i)]
@@ -138,6 +141,11 @@ def lib():
     L.uot_convergence_error.restype = _d
     L.uot_rank_partition.argtypes = [_u64, _u64, _P]
     L.uot_gen_problem_f32.argtypes = [_u64, _u64, _u64, _P, _P, _P, _i]
+    L.uot_gen_block_f32.argtypes = [_u64, _u64, _u64, _u64, _u64, _P, _P, _P, _i]
+    L.uot_host_alloc.argtypes = [_u64]
+    L.uot_host_alloc.restype = _P
+    L.uot_host_free.argtypes = [_P]
+    L.uot_host_free.restype = None
     _lib = L
     return L
 
@@ -233,11 +241,50 @@ def convergence_error(f: ScalingFactors) -> float:
     return lib().uot_convergence_error(_ptr(a), a.size, _ptr(b), b.size)
 
 
-def gen_problem_t(seed: int, m: int, n: int, threads: int = 0) -> Problem:
-    """gen_problem_t<float> (problem_io.hpp:17-31); er = ep = 1."""
+class PinnedBuffer:
+    """Page-locked host array (cudaMallocHost) exposed as a numpy array."""
+
+    def __init__(self, shape, dtype):
+        self.dtype = np.dtype(dtype)
+        n = int(np.prod(shape)) * self.dtype.itemsize
+        self._p = lib().uot_host_alloc(n)
+        if not self._p:
+            raise CudaError(f"cudaMallocHost({n}) failed")
+        self.array = np.ctypeslib.as_array((C.c_uint8 * n).from_address(self._p)).view(self.dtype).reshape(shape)
+
+    def free(self):
+        if self._p:
+            self.array = None
+            lib().uot_host_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def gen_block(seed: int, global_rows: int, n: int, row0: int, rows: int, threads: int = 0,
+              out: np.ndarray | None = None) -> Problem:
+    """Rows [row0, row0+rows) of gen_problem_t<float>(seed, global_rows, n): the
+    rank-local block of a row-sharded problem (A block, rpd slice, full cpd)."""
+    a = np.empty((rows, n), np.float32) if out is None else out
+    rpd = np.empty(rows, np.float64)
+    cpd = np.empty(n, np.float64)
+    rc = lib().uot_gen_block_f32(int(seed), int(global_rows), int(n), int(row0), int(rows), _ptr(a),
+                                 _ptr(rpd), _ptr(cpd), threads or (os.cpu_count() or 1))
+    if rc:
+        _raise(rc, "gen_block: bad block")
+    return Problem(a, rpd, cpd, 1.0, 1.0)
+
+
+def gen_problem_t(seed: int, m: int, n: int, threads: int = 0, out: np.ndarray | None = None) -> Problem:
+    """gen_problem_t<float> (problem_io.hpp:17-31); er = ep = 1. `out` may be a
+    preallocated (m, n) float32 array (e.g. PinnedBuffer.array)."""
     if m < 1 or n < 1:
         _raise(1, "gen_problem: matrix must be at least 1x1")
-    a = np.empty((m, n), np.float32)
+    a = np.empty((m, n), np.float32) if out is None else out
     rpd = np.empty(m, np.float64)
     cpd = np.empty(n, np.float64)
     lib().uot_gen_problem_f32(int(seed), m, n, _ptr(a), _ptr(rpd), _ptr(cpd),
@@ -350,6 +397,16 @@ class Session:
         it, err, conv = _u64(), _d(), _i()
         self._check(lib().uot_iterate(self._h, int(k), float(tol), C.byref(it), C.byref(err), C.byref(conv)))
         return int(it.value), float(err.value), bool(conv.value)
+
+    def iterate_timed(self, k: int = 1, tol: float = 1e-300):
+        """iterate() plus the device milliseconds of the k iterations (CUDA events)."""
+        it, err, conv, ms = _u64(), _d(), _i(), _d()
+        self._check(lib().uot_iterate_timed(self._h, int(k), float(tol), C.byref(it), C.byref(err),
+                                            C.byref(conv), C.byref(ms)))
+        return int(it.value), float(err.value), bool(conv.value), float(ms.value)
+
+    def synchronize(self):
+        self._check(lib().uot_synchronize(self._h))
 
     def factors(self) -> ScalingFactors:
         alpha = np.empty(self.rows, np.float64)

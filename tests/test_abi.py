@@ -1,0 +1,115 @@
+"""The C ABI (include/uot_cuda.h) without a GPU: the library builds, loads and
+exports every declared symbol; the host-side pieces (scalars, partitions, the
+generator) match the reference; the product refuses to run without CUDA (no
+CPU fallback)."""
+from __future__ import annotations
+
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, cuda_ok
+
+HEADER = os.path.join(ROOT, "include", "uot_cuda.h")
+
+
+def declared_symbols():
+    with open(HEADER) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"UOT_API\s+[\w\s\*]+?\b(uot_\w+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def uot():
+    from paper_2412_11079_b200 import uot as u
+    u.lib()
+    return u
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for must in ("uot_create", "uot_create_dist", "uot_set_problem", "uot_init_col_sums", "uot_iterate",
+                 "uot_get_factors", "uot_get_plan", "uot_get_col_sums", "uot_last_error", "uot_destroy"):
+        assert must in syms
+
+
+def test_library_exports_every_declared_symbol(uot):
+    so = uot._build.SO
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(uot_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    lib = uot.lib()
+    for s in declared_symbols():
+        getattr(lib, s)  # resolvable through ctypes
+
+
+def test_library_is_sm100a_code(uot):
+    out = subprocess.run(["cuobjdump", "--list-elf", uot._build.SO], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_sweep_uses_bulk_copies_and_mbarriers(uot):
+    sass = subprocess.run(["cuobjdump", "-sass", uot._build.SO], capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass  # cp.async.bulk (TMA engine) loads and stores
+    assert "SYNCS" in sass   # mbarrier pipeline
+
+
+def test_host_scalars_match_reference(uot, orc):
+    assert uot.compute_fi(1.0, 0.1) == orc.compute_fi(1.0, 0.1)
+    assert uot.compute_fi(3.0, 1.0) == 0.75
+    with pytest.raises(uot.InvalidParameter):
+        uot.compute_fi(0.0, 1.0)
+    assert uot.rescale_factor(8.0, 2.0, 0.5) == 2.0
+    with pytest.raises(uot.DegenerateSum):
+        uot.rescale_factor(1.0, 0.0, 0.5)
+    with pytest.raises(uot.DegenerateSum):
+        uot.rescale_factor(1e300, 1e-300, 1.0)
+    f = uot.ScalingFactors(np.array([4 / 3, 2 / 3]), np.array([1.5, 1.5]))
+    assert uot.convergence_error(f) == pytest.approx(0.5, rel=1e-15)
+
+
+def test_rank_partition(uot, orc):
+    assert uot.RankPartition.make(3, 8).blocks == [(0, 3), (3, 6), (6, 8)]
+    assert [b for b in uot.RankPartition.make(8, 8).blocks] == [(r, r + 1) for r in range(8)]
+    with pytest.raises(uot.PartitionError):
+        uot.RankPartition.make(9, 8)
+    with pytest.raises(uot.PartitionError):
+        uot.RankPartition.make(0, 8)
+    b = orc.rank_partition(7, 131072)
+    assert uot.RankPartition.make(7, 131072).blocks == [(b[i], b[i + 1]) for i in range(7)]
+
+
+def test_host_generator_bit_exact(uot, orc):
+    for seed, m, n in [(42, 257, 129), (7, 1, 1), (3, 5, 4)]:
+        p = uot.gen_problem_t(seed, m, n, threads=3)
+        a, rpd, cpd = orc.gen_problem(seed, m, n)
+        assert np.array_equal(p.a, a) and np.array_equal(p.rpd, rpd) and np.array_equal(p.cpd, cpd)
+
+
+def test_block_generator_is_a_slice_of_the_global_problem(uot, orc):
+    a, rpd, cpd = orc.gen_problem(42, 100, 37)
+    blk = uot.gen_block(42, 100, 37, 30, 45)
+    assert np.array_equal(blk.a, a[30:75]) and np.array_equal(blk.rpd, rpd[30:75])
+    assert np.array_equal(blk.cpd, cpd)
+
+
+@pytest.mark.skipif(cuda_ok(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback(uot):
+    with pytest.raises(uot.CudaError):
+        uot.Session(16, 16)
+    p = uot.gen_problem_t(1, 4, 4)
+    with pytest.raises(uot.CudaError):
+        uot.fused_solve(p, 1e-6, 3)
+
+
+def test_controls_validated_before_any_device_work(uot):
+    # fused.hpp:262-264: tol > 0 and max_iter >= 1 checked up front
+    p = uot.gen_problem_t(1, 4, 4)
+    with pytest.raises(uot.InvalidParameter):
+        uot.fused_solve(p, 0.0, 10)
+    with pytest.raises(uot.InvalidParameter):
+        uot.fused_solve(p, 1e-6, 0)
