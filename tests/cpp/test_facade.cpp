@@ -1,0 +1,175 @@
+// C++ parity suite for the drop-in facade (include/uot/cuda.hpp), written like
+// the reference's own doctest suites (proj/tests/test_fused.cpp,
+// test_distributed.cpp) but against the CUDA backend. It links the UNMODIFIED
+// reference (oracle/_ref, compiled from /root/reference) as the oracle, so it
+// is test infrastructure: built by oracle/Makefile into oracle/_ref/test_facade
+// and run on the GPU box by tests/test_gpu_facade.py. Exit code = failures.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "uot/cuda.hpp"
+#include "uot/fused.hpp"
+#include "uot/problem_io.hpp"
+
+namespace {
+
+int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                       \
+  do {                                                                    \
+    ++g_checks;                                                           \
+    if (!(cond)) {                                                        \
+      ++g_fail;                                                           \
+      std::fprintf(stderr, "%s:%d: CHECK(%s) failed\n", __FILE__, __LINE__, #cond); \
+    }                                                                     \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T)                                          \
+  do {                                                                    \
+    ++g_checks;                                                           \
+    bool ok_ = false;                                                     \
+    try {                                                                 \
+      (void)(expr);                                                       \
+    } catch (const T&) {                                                  \
+      ok_ = true;                                                         \
+    } catch (...) {                                                       \
+    }                                                                     \
+    if (!ok_) {                                                           \
+      ++g_fail;                                                           \
+      std::fprintf(stderr, "%s:%d: %s did not throw %s\n", __FILE__, __LINE__, #expr, #T); \
+    }                                                                     \
+  } while (0)
+
+constexpr double kNever = 1e-300;
+
+uot::Problem<float> random_problem(std::uint64_t seed, std::size_t m, std::size_t n, double fi) {
+  auto p = uot::gen_problem_t<float>(seed, m, n);  // oracle.hpp:61-67
+  p.er = 1.0;
+  p.ep = (1.0 - fi) / fi;
+  return p;
+}
+
+double max_rel(const uot::Matrix<float>& a, const uot::Matrix<float>& b) {
+  double m = 0.0;
+  for (std::size_t k = 0; k < a.size(); ++k)
+    m = std::max(m, std::abs(double(a.data()[k]) - double(b.data()[k])) / std::abs(double(b.data()[k])));
+  return m;
+}
+
+void test_solve_matches_reference() {
+  struct C { std::uint64_t seed; std::size_t m, n; double fi; std::size_t k, w; };
+  for (const C c : {C{21, 16, 16, 0.5, 25, 1}, C{22, 10, 33, 1.0, 25, 1}, C{33, 128, 128, 0.5, 100, 4},
+                    C{42, 1024, 1024, 1 / 1.1, 100, 8}, C{5, 300, 20000, 1 / 1.1, 10, 8}}) {
+    const auto p = random_problem(c.seed, c.m, c.n, c.fi);
+    const auto ref = uot::fused_solve(p, kNever, c.k, c.w);
+    const auto gpu = uot::cuda::fused_solve(p, kNever, c.k);
+    CHECK(gpu.report.iterations == c.k);
+    CHECK(max_rel(gpu.plan, ref.plan) <= 1e-5);
+    CHECK(gpu.plan == ref.plan);  // same arithmetic: bit-identical
+    CHECK(std::abs(gpu.report.final_error - ref.report.final_error) <= 1e-5 * ref.report.final_error);
+    CHECK(uot::max_abs_diff(gpu.factors.alpha, ref.factors.alpha) <= 1e-12);
+    CHECK(uot::max_abs_diff(gpu.factors.beta, ref.factors.beta) <= 1e-12);
+  }
+}
+
+void test_hand_checked_iteration() {  // test_fused.cpp:38-56 in fp32
+  uot::Problem<float> p;
+  p.a = uot::Matrix<float>{{1.f, 1.f}, {1.f, 1.f}};
+  p.rpd = {4.0, 2.0};
+  p.cpd = {3.0, 3.0};
+  uot::Matrix<float> a = p.a;
+  uot::FusedState st{uot::init_col_sums(a)};
+  const auto f = uot::cuda::fused_iterate(a, st, p, 1.0);
+  CHECK(f.beta == std::vector<double>({1.5, 1.5}));
+  CHECK(std::abs(f.alpha[0] - 4.0 / 3.0) <= 1e-15);
+  CHECK(std::abs(f.alpha[1] - 2.0 / 3.0) <= 1e-15);
+  CHECK(a(0, 0) == 2.f && a(1, 1) == 1.f);
+  CHECK(std::abs(st.col_sums[0] - 3.0) <= 1e-14);
+  CHECK(std::abs(uot::convergence_error(f) - 0.5) <= 1e-15);
+}
+
+void test_per_iteration_api_tracks_reference() {
+  const auto p = random_problem(31, 64, 96, 0.5);
+  uot::Matrix<float> mine = p.a, theirs = p.a;
+  uot::FusedState sm{uot::init_col_sums(mine)}, st{uot::init_col_sums(theirs)};
+  for (int it = 0; it < 6; ++it) {
+    const auto fm = uot::cuda::fused_iterate(mine, sm, p, 0.5);
+    const auto ft = uot::fused_iterate(theirs, st, p, 0.5);
+    CHECK(uot::max_abs_diff(fm.alpha, ft.alpha) <= 1e-13);
+  }
+  CHECK(mine == theirs);
+}
+
+void test_session_is_resumable_and_converges() {
+  auto p = random_problem(37, 24, 24, 0.5);
+  double sr = 0, sc = 0;
+  for (double v : p.rpd) sr += v;
+  for (double v : p.cpd) sc += v;
+  for (double& v : p.cpd) v *= sr / sc;  // balanced_problem (oracle.hpp:74-83)
+  const auto ref = uot::fused_solve(p, 1e-6, 10000);
+  uot::cuda::Session s(24, 24);
+  s.set_problem(p);
+  s.init_col_sums();
+  std::size_t total = 0;
+  bool conv = false;
+  while (!conv && total < 10000) {
+    const auto pr = s.iterate(7, 1e-6);
+    total += pr.iterations;
+    conv = pr.converged;
+  }
+  CHECK(ref.report.converged && conv);
+  CHECK(total == ref.report.iterations);
+  CHECK(max_rel(s.plan(), ref.plan) <= 1e-5);
+}
+
+void test_errors_map_to_reference_exceptions() {
+  const auto p = random_problem(38, 4, 4, 0.5);
+  CHECK_THROWS_AS(uot::cuda::fused_solve(p, 0.0, 10), uot::InvalidParameter);
+  CHECK_THROWS_AS(uot::cuda::fused_solve(p, 1e-6, 0), uot::InvalidParameter);
+  uot::Matrix<float> a = p.a;
+  uot::FusedState zero{std::vector<double>(4, 0.0)};
+  CHECK_THROWS_AS(uot::cuda::fused_iterate(a, zero, p, 0.5), uot::DegenerateSum);
+  uot::FusedState bad_len{std::vector<double>(3, 1.0)};
+  CHECK_THROWS_AS(uot::cuda::fused_iterate(a, bad_len, p, 0.5), uot::InvalidParameter);
+  auto broken = p;
+  broken.a(0, 0) = -1.f;
+  CHECK_THROWS_AS(uot::cuda::fused_solve(broken, 1e-6, 10), uot::InvalidParameter);
+  std::uint8_t id[128] = {0};
+  CHECK_THROWS_AS(uot::cuda::distributed_solve(p, 1e-6, 10, 0, 5, id, 0), uot::PartitionError);
+}
+
+void test_single_rank_distributed() {  // test_distributed.cpp:92-104, 142-155
+  const auto p = random_problem(24, 64, 64, 0.5);
+  std::uint8_t id[128] = {0};
+  const auto d = uot::cuda::distributed_solve(p, kNever, 37, 0, 1, id, 0);
+  const auto ref = uot::distributed_solve(p, kNever, 37, std::size_t(1));
+  CHECK(d.report.iterations == 37 && d.report.solver == "dist");
+  CHECK(d.comm.allreduce_calls == 37 && d.comm.doubles_reduced == 37u * 64u);
+  CHECK(max_rel(d.plan, ref.plan) <= 1e-5);
+}
+
+}  // namespace
+
+int main() {
+  const std::vector<std::pair<const char*, std::function<void()>>> cases = {
+      {"solve matches the reference", test_solve_matches_reference},
+      {"hand-checked iteration", test_hand_checked_iteration},
+      {"per-iteration API", test_per_iteration_api_tracks_reference},
+      {"session resumable + converges", test_session_is_resumable_and_converges},
+      {"errors", test_errors_map_to_reference_exceptions},
+      {"single-rank distributed", test_single_rank_distributed},
+  };
+  for (const auto& [name, fn] : cases) {
+    const int before = g_fail;
+    try {
+      fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::fprintf(stderr, "%s: unexpected exception: %s\n", name, e.what());
+    }
+    std::printf("%-34s %s\n", name, g_fail == before ? "PASS" : "FAIL");
+  }
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail;
+}
