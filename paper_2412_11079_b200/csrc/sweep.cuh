@@ -112,55 +112,78 @@ __device__ __forceinline__ float& comp(float4& v, int e) {
   return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
 }
 
+// Chunks are processed in groups of KG float4 (8 values for KG = 2): one screen
+// and one branch per group keeps the fast path branch-light while bounding the
+// live registers (V = 4 would otherwise spill under the 96-register cap of a
+// 19-warp CTA).
+template <int V>
+struct ChunkGroup {
+  static constexpr int KG = (V <= 2 || V % 2 != 0) ? V : 2;
+  static constexpr int NG = V / KG;
+  static_assert(V % KG == 0, "V must be a multiple of the chunk group");
+};
+
 // fused.hpp:125-131 for this thread's part of one row: x <- f32(f64(x)*beta_j),
 // returns the f64 sum of the stored values; `x1bad` when a stored value is not
 // positive normal (sweep 2 then converts this row exactly).
 template <int NT, int V, bool FULL>
 __device__ __forceinline__ double row_sweep1(float4* row, unsigned tid, unsigned nq, const double* beta,
                                              bool& x1bad) {
-  float4 v[V];
-  uint32_t m = 0;
-#pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const unsigned q = tid + k * NT;
-    v[k] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[k], e));
-  }
-  if (nn_ok(m)) {
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) comp(v[k], e) = d2f(fastd(comp(v[k], e)) * beta[4 * k + e]);
-  } else {
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        comp(v[k], e) = d2f(static_cast<double>(comp(v[k], e)) * beta[4 * k + e]);
-  }
-  uint32_t m1 = 0;
+  constexpr int KG = ChunkGroup<V>::KG;
   double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const unsigned q = tid + k * NT;
-    if (FULL || q < nq) {
-      row[q] = v[k];
+  for (int g0 = 0; g0 < V; g0 += KG) {
+    float4 v[KG];
+    uint32_t m = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        m1 = nn_max(m1, comp(v[k], e));
-        s[e] += fastd(comp(v[k], e));
+    for (int kk = 0; kk < KG; ++kk) {
+      const unsigned q = tid + (g0 + kk) * NT;
+      v[kk] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[kk], e));
+    }
+    if (nn_ok(m)) {
+#pragma unroll
+      for (int kk = 0; kk < KG; ++kk)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(fastd(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < KG; ++kk)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          comp(v[kk], e) = d2f(static_cast<double>(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
+    }
+    uint32_t m1 = 0;
+    double t[4];
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) {
+      const unsigned q = tid + (g0 + kk) * NT;
+      if (FULL || q < nq) {
+        row[q] = v[kk];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          m1 = nn_max(m1, comp(v[kk], e));
+          const double x = fastd(comp(v[kk], e));
+          t[e] = kk == 0 ? x : t[e] + x;
+        }
+      } else if (kk == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t[e] = 0.0;
       }
     }
-  }
-  if (!nn_ok(m1)) {
-    x1bad = true;
-    s[0] = s[1] = s[2] = s[3] = 0.0;
+    if (!nn_ok(m1)) {
+      x1bad = true;
 #pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (FULL || tid + k * NT < nq)
+      for (int e = 0; e < 4; ++e) t[e] = 0.0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) s[e] += static_cast<double>(comp(v[k], e));
+      for (int kk = 0; kk < KG; ++kk)
+        if (FULL || tid + (g0 + kk) * NT < nq)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) t[e] += static_cast<double>(comp(v[kk], e));
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[e] = g0 == 0 ? t[e] : s[e] + t[e];
   }
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
@@ -170,72 +193,80 @@ __device__ __forceinline__ double row_sweep1(float4* row, unsigned tid, unsigned
 template <int NT, int V, bool FULL>
 __device__ __forceinline__ void row_sweep2(float4* row, unsigned tid, unsigned nq, double al, bool x1bad,
                                            double* acc) {
-  float4 v[V];
+  constexpr int KG = ChunkGroup<V>::KG;
 #pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const unsigned q = tid + k * NT;
-    v[k] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
-  }
-  if (!x1bad) {
+  for (int g0 = 0; g0 < V; g0 += KG) {
+    float4 v[KG];
 #pragma unroll
-    for (int k = 0; k < V; ++k)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) comp(v[k], e) = d2f(fastd(comp(v[k], e)) * al);
-  } else {
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) comp(v[k], e) = d2f(static_cast<double>(comp(v[k], e)) * al);
-  }
-  uint32_t m2 = 0;
-#pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const unsigned q = tid + k * NT;
-    if (FULL || q < nq) {
-      row[q] = v[k];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) m2 = nn_max(m2, comp(v[k], e));
+    for (int kk = 0; kk < KG; ++kk) {
+      const unsigned q = tid + (g0 + kk) * NT;
+      v[kk] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
     }
-  }
-  if (nn_ok(m2)) {
+    if (!x1bad) {
 #pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (FULL || tid + k * NT < nq)
+      for (int kk = 0; kk < KG; ++kk)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[4 * k + e] += fastd(comp(v[k], e));
-  } else {
+        for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(fastd(comp(v[kk], e)) * al);
+    } else {
 #pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (FULL || tid + k * NT < nq)
+      for (int kk = 0; kk < KG; ++kk)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[4 * k + e] += static_cast<double>(comp(v[k], e));
+        for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(static_cast<double>(comp(v[kk], e)) * al);
+    }
+    uint32_t m2 = 0;
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) {
+      const unsigned q = tid + (g0 + kk) * NT;
+      if (FULL || q < nq) {
+        row[q] = v[kk];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m2 = nn_max(m2, comp(v[kk], e));
+      }
+    }
+    if (nn_ok(m2)) {
+#pragma unroll
+      for (int kk = 0; kk < KG; ++kk)
+        if (FULL || tid + (g0 + kk) * NT < nq)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += fastd(comp(v[kk], e));
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < KG; ++kk)
+        if (FULL || tid + (g0 + kk) * NT < nq)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(v[kk], e));
+    }
   }
 }
 
 // fused.hpp:96-110 seed: next_j += f64(x) over the stored values.
 template <int NT, int V, bool FULL>
 __device__ __forceinline__ void row_seed(const float4* row, unsigned tid, unsigned nq, double* acc) {
-  float4 v[V];
-  uint32_t m = 0;
+  constexpr int KG = ChunkGroup<V>::KG;
 #pragma unroll
-  for (int k = 0; k < V; ++k) {
-    const unsigned q = tid + k * NT;
-    v[k] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
+  for (int g0 = 0; g0 < V; g0 += KG) {
+    float4 v[KG];
+    uint32_t m = 0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[k], e));
-  }
-  if (nn_ok(m)) {
+    for (int kk = 0; kk < KG; ++kk) {
+      const unsigned q = tid + (g0 + kk) * NT;
+      v[kk] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
 #pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (FULL || tid + k * NT < nq)
+      for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[kk], e));
+    }
+    if (nn_ok(m)) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[4 * k + e] += fastd(comp(v[k], e));
-  } else {
+      for (int kk = 0; kk < KG; ++kk)
+        if (FULL || tid + (g0 + kk) * NT < nq)
 #pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (FULL || tid + k * NT < nq)
+          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += fastd(comp(v[kk], e));
+    } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[4 * k + e] += static_cast<double>(comp(v[k], e));
+      for (int kk = 0; kk < KG; ++kk)
+        if (FULL || tid + (g0 + kk) * NT < nq)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(v[kk], e));
+    }
   }
 }
 
