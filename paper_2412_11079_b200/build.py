@@ -61,7 +61,19 @@ def build_trace() -> str:
     return TRACE_SO
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experiment builds (phase timers, pipeline-only) next to the product .so."""
+    out = os.path.join(PKG, f"libuot_cuda_{name}.so")
+    r = subprocess.run(nvcc_cmd(out, [f"-D{d}" for d in defines]), capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed building the {name} variant")
+    return out
+
+
 if __name__ == "__main__":
     if "--trace" in sys.argv:
         build_trace()
+    if "--pipe" in sys.argv:
+        build_variant("pipe", ["UOT_PIPE_ONLY"])
     build(force="--force" in sys.argv, verbose="--quiet" not in sys.argv)

@@ -285,10 +285,10 @@ struct SweepSmem {
 // ring slots. LA: batches between sweep 1 and sweep 2 of a batch beyond the
 // next one (the factor warps' latency budget). XCHG: G > 1, row sums are
 // exchanged across the group. SEED: the read-only init_col_sums sweep.
-template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, bool FULL, bool SEED>
-__global__ void __launch_bounds__(NT + 32 * (XCHG ? 3 : 2), 1) sweep_kernel(const SweepArgs a) {
+template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED>
+__global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const SweepArgs a) {
   constexpr int NW = NT / 32;
-  constexpr int NF = XCHG ? 2 : 1;  // factor warps
+  static_assert(NF >= 1 && NF <= 2, "factor warps");
   static_assert(LA >= 1 && LA <= 2 && (!XCHG || LA == 2), "lag");
   static_assert(NBUF >= LA + 4, "ring too small");
   static_assert(!XCHG || BM == 1, "the exchange path moves one row per batch");
@@ -542,7 +542,11 @@ __global__ void __launch_bounds__(NT + 32 * (XCHG ? 3 : 2), 1) sweep_kernel(cons
         part[r] = 0.0;
         if (r < static_cast<int>(nr)) {
           bool bad = false;
+#ifdef UOT_PIPE_ONLY
+          part[r] = 1.0;
+#else
           part[r] = row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, bad);
+#endif
           if (bad) x1bad |= 1u << (shift + r);
         }
       }
@@ -562,9 +566,15 @@ __global__ void __launch_bounds__(NT + 32 * (XCHG ? 3 : 2), 1) sweep_kernel(cons
       const uint32_t shift = (b % 4) * 8;
 #pragma unroll
       for (int r = 0; r < BM; ++r) {
+#ifndef UOT_PIPE_ONLY
         if (r < static_cast<int>(nr))
           row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq,
                                   alpha_s[qb * BM + r], (x1bad >> (shift + r)) & 1u, acc);
+#else
+        if (r < static_cast<int>(nr))
+#pragma unroll
+          for (int i = 0; i < 4 * V; ++i) acc[i] += 1.0;
+#endif
       }
       fence_proxy_async_smem();  // generic writes -> the producer's bulk store
       __syncwarp();

@@ -30,28 +30,32 @@ constexpr unsigned kSliceMaxXchg = 8192;  // ... when a row spans G > 1 CTAs
 // ------------------------------------------------------------ kernel table --
 using SweepFn = void (*)(const SweepArgs);
 struct SweepCfg {
-  int nt, v, bm, nbuf;
+  int nt, v, bm, nbuf, nf;
   bool xchg;           // rows span G > 1 CTAs (cross-CTA row-sum exchange)
   SweepFn iter[2];     // [FULL]
   SweepFn seed[2];     // [FULL]
   size_t (*smem_bytes)(unsigned buf_stride);
 };
 
-// G == 1: sweep 2 lags sweep 1 by LA=1 extra batch (the factor warp's budget).
-// G > 1: LA=2, the row partials are gathered one batch after publication.
+// G == 1: sweep 2 lags sweep 1 by LA=1 extra batch (the factor warps' budget).
+// G > 1: LA=2, the row partials are exchanged across the group.
+// NF factor warps alternate batches: 2 when a batch is one row (a pow and, for
+// G > 1, an L2 round trip per batch), else 1 (the B rows of a batch run on lanes).
 template <int NT, int V, int BM, int NB, bool XCHG = false>
 SweepCfg make_cfg() {
   constexpr int LA = XCHG ? 2 : 1;
+  constexpr int NF = (XCHG || BM == 1) ? 2 : 1;
   SweepCfg c{};
   c.nt = NT;
   c.v = V;
   c.bm = BM;
   c.nbuf = NB;
+  c.nf = NF;
   c.xchg = XCHG;
-  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, false, false>;
-  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, true, false>;
-  c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, false, true>;
-  c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, true, true>;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false>;
+  c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true>;
+  c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
   return c;
 }
@@ -310,7 +314,7 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctx->grid);
   // compute warps + producer warp + factor warp(s)
-  lc.blockDim = dim3(ctx->cfg->nt + (!seed && ctx->cfg->xchg ? 96 : 64));
+  lc.blockDim = dim3(ctx->cfg->nt + 32 * (1 + (seed ? 1 : ctx->cfg->nf)));
   lc.dynamicSmemBytes = ctx->smem;
   lc.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
@@ -513,7 +517,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->G = ctx->G;
   o->groups = ctx->groups;
   o->rows_per_step = ctx->B;
-  o->threads = ctx->cfg->nt + (ctx->cfg->xchg ? 96 : 64);
+  o->threads = ctx->cfg->nt + 32 * (1 + ctx->cfg->nf);
   o->chunks = ctx->cfg->v;
   o->smem_bytes = static_cast<uint32_t>(ctx->smem);
   o->nbuf = ctx->cfg->nbuf;
