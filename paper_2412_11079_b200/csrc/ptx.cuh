@@ -119,6 +119,13 @@ __device__ __forceinline__ void ld_relaxed_b128(const void* p, unsigned long lon
       : "memory");
 }
 
+// 128-bit global store that streams past L1 and carries an L2 eviction hint.
+__device__ __forceinline__ void st_global_v4(float4* p, float4 v, uint64_t policy) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(policy)
+               : "memory");
+}
+
 // mbarrier arrive (count 1, release at CTA scope) and a parity wait that backs off.
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");

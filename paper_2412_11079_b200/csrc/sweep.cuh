@@ -50,7 +50,7 @@ struct SweepArgs {
   const double* rpd;          // [rows] row marginals
   double* alpha;              // [rows] row factors (output)
   double* partials;           // [groups][pitch] column partials (output)
-  double* cta_err;            // [grid][2] max|alpha-1| seen by each CTA's factor warps (output)
+  double* cta_err;            // [grid][kErrSlots] max|alpha-1| seen by each CTA's factor warps (output)
   ulonglong2* xrec;           // [grid][kRing] exchanged {partial bits, tag} (G > 1)
   Control* ctl;
   unsigned long long rows;    // local rows
@@ -189,10 +189,11 @@ __device__ __forceinline__ double row_sweep1(float4* row, unsigned tid, unsigned
 }
 
 // fused.hpp:135-142 for this thread's part of one row: x <- f32(f64(x)*alpha),
-// next_j += f64(x).
+// next_j += f64(x). The result goes back to the smem slot (bulk-stored by the
+// producer) or, with `grow`, straight to HBM with 128-bit streaming stores.
 template <int NT, int V, bool FULL>
-__device__ __forceinline__ void row_sweep2(float4* row, unsigned tid, unsigned nq, double al, bool x1bad,
-                                           double* acc) {
+__device__ __forceinline__ void row_sweep2(float4* row, float4* grow, uint64_t pol, unsigned tid, unsigned nq,
+                                           double al, bool x1bad, double* acc) {
   constexpr int KG = ChunkGroup<V>::KG;
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
@@ -218,7 +219,10 @@ __device__ __forceinline__ void row_sweep2(float4* row, unsigned tid, unsigned n
     for (int kk = 0; kk < KG; ++kk) {
       const unsigned q = tid + (g0 + kk) * NT;
       if (FULL || q < nq) {
-        row[q] = v[kk];
+        if (grow)
+          st_global_v4(grow + q, v[kk], pol);
+        else
+          row[q] = v[kk];
 #pragma unroll
         for (int e = 0; e < 4; ++e) m2 = nn_max(m2, comp(v[kk], e));
       }
@@ -284,13 +288,21 @@ struct SweepSmem {
 // thread per row (slice <= 4*NT*V; FULL: equality), BM max rows per batch, NBUF
 // ring slots. LA: batches between sweep 1 and sweep 2 of a batch beyond the
 // next one (the factor warps' latency budget). XCHG: G > 1, row sums are
-// exchanged across the group. SEED: the read-only init_col_sums sweep.
-template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED>
+// exchanged across the group. SEED: the read-only init_col_sums sweep. STG:
+// sweep 2 stores straight to HBM from registers, so a slot is refilled as soon
+// as sweep 2 has read it (one slot more of lag for the same ring).
+template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED, bool STG = false>
 __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const SweepArgs a) {
   constexpr int NW = NT / 32;
-  static_assert(NF >= 1 && NF <= 2, "factor warps");
-  static_assert(LA >= 1 && LA <= 2 && (!XCHG || LA == 2), "lag");
-  static_assert(NBUF >= LA + 4, "ring too small");
+  static_assert(NF >= 1 && NF <= kErrSlots, "factor warps");
+  static_assert(LA >= 1 && LA <= 3 && (!XCHG || LA >= 2), "lag");
+  static_assert(NBUF >= LA + (STG ? 3 : 4), "ring too small");
+#ifdef UOT_EARLY_DONE1
+  constexpr bool EARLY_DONE1 = true;
+#else
+  constexpr bool EARLY_DONE1 = false;
+#endif
+  static_assert(!EARLY_DONE1 || LA <= kQ - 2, "alpha/red rings too short for an early done1");
   static_assert(!XCHG || BM == 1, "the exchange path moves one row per batch");
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -382,7 +394,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       TR_BEGIN();
       mbar_wait(&done2[b % NBUF], (b / NBUF) & 1u);  // slot b consumed (sweep 2 / seed done)
       TR_END(4);
-      if (SEED) {
+      if (SEED || STG) {
         if (b + NBUF < nb) issue_load(b + NBUF);
         continue;
       }
@@ -399,7 +411,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         TR_END(7);
       }
     }
-    if (!SEED) bulk_wait<0>();  // every store landed before the CTA retires
+    if (!SEED && !STG) bulk_wait<0>();  // every store landed before the CTA retires
 #ifdef UOT_TRACE
     tr_acc[8] = clock64() - tr_p0;
     TR_FLUSH(4, 9);
@@ -428,6 +440,12 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       TR_BEGIN();
       mbar_wait(&done1[q], (s / kQ) & 1u);
       TR_END(0);
+#ifdef UOT_NO_FACTOR
+      if (lane < static_cast<int>(nr)) alpha_s[q * BM + lane] = 1.0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&alpha_rdy[q]);
+      continue;
+#endif
       TR_BEGIN();
       double t = 0.0;  // this CTA's partial of row `lane` of the batch, warp order
       if (lane < static_cast<int>(nr)) {
@@ -435,24 +453,39 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
 #pragma unroll
         for (int w = 1; w < NW; ++w) t += red[(q * NW + w) * BM + lane];
       }
+#ifdef UOT_NO_XCHG
+      if (false) {
+#else
       if (XCHG) {
+#endif
         // Publish {partial, tag} for the group, then gather all G partials of
         // the row and sum them in ascending g (identical bits on every CTA).
+#ifdef UOT_XREC_GROUPED
+        // the G records of one row are adjacent: one 16*G-byte poll per round trip
+        ulonglong2* const xrow = &a.xrec[(static_cast<size_t>(group) * kRing + (s % kRing)) * G];
+        ulonglong2* const xmine = xrow + g;
+        const ulonglong2* const xpeer = xrow + lane;
+#else
+        ulonglong2* const xmine = &a.xrec[static_cast<size_t>(blockIdx.x) * kRing + (s % kRing)];
+        const ulonglong2* const xpeer = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (s % kRing)];
+#endif
         if (lane == 0)
-          st_relaxed_b128(&a.xrec[static_cast<size_t>(blockIdx.x) * kRing + (s % kRing)],
+          st_relaxed_b128(xmine,
                           static_cast<unsigned long long>(__double_as_longlong(t)), tag_hi | (s + 1));
         TR_END(1);
         TR_BEGIN();
         double v = 0.0;
         if (lane < static_cast<int>(G)) {
-          const ulonglong2* rec = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (s % kRing)];
+          const ulonglong2* rec = xpeer;
           const unsigned long long want = tag_hi | (s + 1);
           unsigned long long lo, hi;
           ld_relaxed_b128(rec, lo, hi);
           if (hi != want) {
             const unsigned long long t0 = globaltimer_ns();
             do {
+#ifdef UOT_POLL_SLEEP
               __nanosleep(32);
+#endif
               ld_relaxed_b128(rec, lo, hi);
               if (hi != want && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
                 atomicOr(&ctl->status, kStatusExchangeTimeout);
@@ -470,7 +503,12 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       }
       if (lane < static_cast<int>(nr)) {
         double al;
+#ifdef UOT_NO_POW
+        al = t > 0 ? 1.0 : rv;
+        if (false) {
+#else
         if (!rescale_factor_dev(rv, t, a.fi, &al)) {
+#endif
           atomicOr(&ctl->alpha_bad, 1);
           al = 1.0;
         }
@@ -486,8 +524,9 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     }
     for (int o = 16; o > 0; o >>= 1) errmax = fmax(errmax, __shfl_xor_sync(0xffffffffu, errmax, o));
     if (lane == 0) {
-      a.cta_err[2 * blockIdx.x + f] = errmax;
-      if (NF == 1) a.cta_err[2 * blockIdx.x + 1] = 0.0;
+      a.cta_err[kErrSlots * blockIdx.x + f] = errmax;
+      if (f == 0)
+        for (int k = NF; k < kErrSlots; ++k) a.cta_err[kErrSlots * blockIdx.x + k] = 0.0;
     }
 #ifdef UOT_TRACE
     tr_acc[9] = clock64() - tr_f0;
@@ -497,6 +536,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   }
 
   // ========================================================= compute warps ==
+  const uint64_t spol = a.evict_first ? policy_evict_first() : policy_evict_normal();
   double beta[4 * V], acc[4 * V];
 #pragma unroll
   for (int i = 0; i < 4 * V; ++i) acc[i] = 0.0;
@@ -510,15 +550,33 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     }
   }
 
-  uint32_t x1bad = 0;  // bit (b % 4) * 8 + r: row r of batch b stored a non-normal x1
+  uint64_t x1bad = 0;  // bit (b % 8) * 8 + r: row r of batch b stored a non-normal x1
 #ifdef UOT_TRACE
   const unsigned long long tr_c0 = clock64();
 #endif
   const unsigned nsteps = SEED ? nb : nb + LA + 1;
+  double part[BM];
+  // Row partials of batch s: warp xor-tree -> smem -> done1 (the factor warps).
+  auto reduce_rows = [&](unsigned s) {
+    if (SEED || s >= nb) return;
+    TR_BEGIN();
+    const unsigned nr = rows_in(s);
+    const unsigned qq = s % kQ;
+#pragma unroll
+    for (int r = 0; r < BM; ++r) {
+      if (r < static_cast<int>(nr)) {
+        const double t = warp_sum(part[r]);
+        if (lane == 0) red[(qq * NW + warp) * BM + r] = t;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done1[qq]);
+    TR_END(18);
+  };
   for (unsigned s = 0; s < nsteps; ++s) {
     // sweep 1 on batch s (or the seed accumulation); its row partials are
-    // reduced after sweep 2 below so the shuffle latency overlaps that work.
-    double part[BM];
+    // reduced before (EARLY_DONE1: the factor chain starts sooner) or after
+    // sweep 2 (the shuffle latency overlaps that work).
     if (s < nb) {
       TR_BEGIN();
       mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
@@ -535,8 +593,8 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         if (lane == 0) mbar_arrive(&done2[s % NBUF]);
         continue;
       }
-      const uint32_t shift = (s % 4) * 8;
-      x1bad &= ~(0xffu << shift);
+      const uint32_t shift = (s % 8) * 8;
+      x1bad &= ~(0xffull << shift);
 #pragma unroll
       for (int r = 0; r < BM; ++r) {
         part[r] = 0.0;
@@ -547,11 +605,13 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
 #else
           part[r] = row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, bad);
 #endif
-          if (bad) x1bad |= 1u << (shift + r);
+          if (bad) x1bad |= 1ull << (shift + r);
         }
       }
       TR_END(17);
     }
+
+    if (EARLY_DONE1) reduce_rows(s);
 
     // sweep 2 on batch s-1-LA once its factors are published.
     if (!SEED && s >= static_cast<unsigned>(LA + 1) && s - (LA + 1) < nb) {
@@ -563,40 +623,28 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       TR_BEGIN();
       float* buf = slot_ptr(b);
       const unsigned nr = rows_in(b);
-      const uint32_t shift = (b % 4) * 8;
+      const uint32_t shift = (b % 8) * 8;
 #pragma unroll
       for (int r = 0; r < BM; ++r) {
 #ifndef UOT_PIPE_ONLY
         if (r < static_cast<int>(nr))
-          row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq,
-                                  alpha_s[qb * BM + r], (x1bad >> (shift + r)) & 1u, acc);
+          row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice),
+                                  STG ? reinterpret_cast<float4*>(gbase + (static_cast<size_t>(b) * B + r) * a.pitch)
+                                      : nullptr,
+                                  spol, tid, nq, alpha_s[qb * BM + r], (x1bad >> (shift + r)) & 1ull, acc);
 #else
         if (r < static_cast<int>(nr))
 #pragma unroll
           for (int i = 0; i < 4 * V; ++i) acc[i] += 1.0;
 #endif
       }
-      fence_proxy_async_smem();  // generic writes -> the producer's bulk store
+      if (!STG) fence_proxy_async_smem();  // generic writes -> the producer's bulk store
       __syncwarp();
       if (lane == 0) mbar_arrive(&done2[b % NBUF]);
       TR_END(20);
     }
 
-    if (!SEED && s < nb) {
-      TR_BEGIN();
-      const unsigned nr = rows_in(s);
-      const unsigned qq = s % kQ;
-#pragma unroll
-      for (int r = 0; r < BM; ++r) {
-        if (r < static_cast<int>(nr)) {
-          const double t = warp_sum(part[r]);
-          if (lane == 0) red[(qq * NW + warp) * BM + r] = t;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&done1[qq]);
-      TR_END(18);
-    }
+    if (!EARLY_DONE1) reduce_rows(s);
   }
 #ifdef UOT_TRACE
   tr_acc[21] = clock64() - tr_c0;

@@ -41,10 +41,25 @@ struct SweepCfg {
 // G > 1: LA=2, the row partials are exchanged across the group.
 // NF factor warps alternate batches: 2 when a batch is one row (a pow and, for
 // G > 1, an L2 round trip per batch), else 1 (the B rows of a batch run on lanes).
+#ifndef UOT_LA_G1
+#define UOT_LA_G1 2
+#endif
+#ifndef UOT_LA_X
+#define UOT_LA_X 2
+#endif
+#ifndef UOT_NF_X
+#define UOT_NF_X 2
+#endif
+#ifndef UOT_STG
+#define UOT_STG 0
+#endif
 template <int NT, int V, int BM, int NB, bool XCHG = false>
 SweepCfg make_cfg() {
-  constexpr int LA = XCHG ? 2 : 1;
-  constexpr int NF = (XCHG || BM == 1) ? 2 : 1;
+  constexpr int LA = XCHG ? UOT_LA_X : UOT_LA_G1;
+#ifndef UOT_NF_G1
+#define UOT_NF_G1 3
+#endif
+  constexpr int NF = XCHG ? UOT_NF_X : UOT_NF_G1;
   SweepCfg c{};
   c.nt = NT;
   c.v = V;
@@ -52,8 +67,8 @@ SweepCfg make_cfg() {
   c.nbuf = NB;
   c.nf = NF;
   c.xchg = XCHG;
-  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false>;
-  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false>;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false, UOT_STG>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false, UOT_STG>;
   c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true>;
   c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
@@ -239,7 +254,7 @@ int alloc_all(uot_ctx* ctx) {
   if ((rc = dalloc(ctx, &ctx->col_sums, pitch))) return rc;
   if ((rc = dalloc(ctx, &ctx->xsum, pitch + ctx->nranks))) return rc;
   if ((rc = dalloc(ctx, &ctx->partials, static_cast<size_t>(ctx->groups) * pitch))) return rc;
-  if ((rc = dalloc(ctx, &ctx->cta_err, 2 * static_cast<size_t>(ctx->grid)))) return rc;
+  if ((rc = dalloc(ctx, &ctx->cta_err, kErrSlots * static_cast<size_t>(ctx->grid)))) return rc;
   const size_t xn = static_cast<size_t>(ctx->grid) * kRing;
   if ((rc = dalloc(ctx, &ctx->xrec, xn))) return rc;
   if ((rc = dalloc(ctx, &ctx->ctl, 1))) return rc;
@@ -260,6 +275,7 @@ int create_common(uot_ctx* ctx, int device) {
     return ctx->fail(UOT_INVALID_PARAMETER, "device %d out of range (%d visible)", device, ndev);
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
+  ctx->sms = std::max(1, std::min(ctx->sms, env_int("UOT_SMS", ctx->sms)));  // experiments: cap the grid
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   int rc = plan_layout(ctx);
   if (rc) return rc;
@@ -328,9 +344,9 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
 
 template <int MODE>
 int launch_finalize_single(uot_ctx* ctx) {
-  const unsigned blocks = (ctx->pitch + 255) / 256;
+  const unsigned blocks = finalize_blocks(ctx->pitch);
   ctx->launches++;
-  finalize_kernel<MODE, true, true><<<blocks, 256, 0, ctx->stream>>>(fin_args(ctx));
+  finalize_kernel<MODE, true, true><<<blocks, kFinThreads, 0, ctx->stream>>>(fin_args(ctx));
   return ctx->cuda(cudaGetLastError(), "finalize launch");
 }
 
@@ -342,17 +358,17 @@ int nccl_check(uot_ctx* ctx, ncclResult_t r, const char* what) {
 // Multi-GPU tail: local reduce -> one allreduce of cols + nranks doubles -> beta.
 template <int MODE>
 int launch_finalize_dist(uot_ctx* ctx) {
-  const unsigned blocks = (ctx->pitch + 255) / 256;
+  const unsigned blocks = finalize_blocks(ctx->pitch);
   const FinalizeArgs f = fin_args(ctx);
   ctx->launches += 2;
-  finalize_kernel<MODE, true, false><<<blocks, 256, 0, ctx->stream>>>(f);
+  finalize_kernel<MODE, true, false><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
   int rc = ctx->cuda(cudaGetLastError(), "finalize(reduce) launch");
   if (rc) return rc;
   rc = nccl_check(ctx, nccl().AllReduce(ctx->xsum, ctx->xsum, ctx->cols + ctx->nranks, ncclFloat64,
                                         ncclSum, ctx->comm, ctx->stream),
                   "ncclAllReduce");
   if (rc) return rc;
-  finalize_kernel<MODE, false, true><<<blocks, 256, 0, ctx->stream>>>(f);
+  finalize_kernel<MODE, false, true><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
   return ctx->cuda(cudaGetLastError(), "finalize(beta) launch");
 }
 
@@ -606,9 +622,9 @@ int uot_set_col_sums(uot_ctx* ctx, const double* col_sums) {
   // Recompute beta(iter+1) from the given state; its error slot starts at zero.
   CK(cudaMemsetAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Control, err_beta), 0,
                      2 * sizeof(double), ctx->stream));
-  const unsigned blocks = (ctx->pitch + 255) / 256;
+  const unsigned blocks = finalize_blocks(ctx->pitch);
   ctx->launches++;
-  finalize_kernel<kFinBetaOnly, false, true><<<blocks, 256, 0, ctx->stream>>>(fin_args(ctx));
+  finalize_kernel<kFinBetaOnly, false, true><<<blocks, kFinThreads, 0, ctx->stream>>>(fin_args(ctx));
   CK(cudaGetLastError());
   int rc = sync_ctl(ctx);
   if (rc) return rc;

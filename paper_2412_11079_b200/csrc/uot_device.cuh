@@ -8,6 +8,7 @@ namespace uotk {
 constexpr int kStatusDegenerateAlpha = 1;   // rescale_factor threw for a row (scaling.cpp:15-22)
 constexpr int kStatusDegenerateBeta = 2;    // beta_from_state threw (fused.hpp:146-157)
 constexpr int kStatusExchangeTimeout = 4;   // a peer CTA never published (co-residency bug)
+constexpr int kErrSlots = 4;                // max|alpha-1| slots per sweep CTA (one per factor warp)
 constexpr unsigned long long kExchangeTimeoutNs = 4000000000ull;
 
 // One per session, in device memory. Written only by kernels between launches
@@ -44,7 +45,11 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 __device__ __forceinline__ bool rescale_factor_dev(double target, double sum, double fi,
                                                    double* out) {
   if (!(sum > 0.0)) return false;
+#ifdef UOT_FAST_POW
+  const double f = exp2(fi * log2(target / sum));
+#else
   const double f = pow(target / sum, fi);
+#endif
   if (!(f > 0.0) || !isfinite(f)) return false;
   *out = f;
   return true;

@@ -1,0 +1,25 @@
+"""Device time of the sweep per shape for one library build (scratch tool).
+
+UOT_LIB_PATH=paper_2412_11079_b200/libuot_cuda_pipe.so python tools/time_shapes.py 32768x32768x20 ...
+"""
+import os
+import sys
+
+sys.path.insert(0, ".")
+from paper_2412_11079_b200 import uot  # noqa: E402
+
+tag = os.path.basename(os.environ.get("UOT_LIB_PATH", "libuot_cuda.so"))
+for spec in sys.argv[1:]:
+    m, n, k = (int(x) for x in spec.split("x"))
+    with uot.Session(m, n) as s:
+        s.generate_problem(42, 1.0, 0.1)
+        s.init_col_sums()
+        s.set_timing(True)
+        s.iterate(3, 1e-300)
+        s.iterate(k, 1e-300)
+        sw, fin, n_ = s.timing()
+        gbs = 2 * m * n * 4 / (sw / n_ * 1e-3) / 1e9
+        lay = s.layout
+        print(f"[{tag}] {m}x{n}: sweep {sw / n_ * 1e3:.1f} us ({gbs:.0f} GB/s) finalize {fin / n_ * 1e3:.1f} us "
+              f"G={lay['G']} groups={lay['groups']} B={lay['rows_per_step']} thr={lay['threads']} v={lay['chunks']}",
+              flush=True)
