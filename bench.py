@@ -225,12 +225,9 @@ def run_ours(args, grp: Group):
     world, rank = grp.world, grp.rank
     rows_global = ROWS_PER_GPU * world
     units = (rows_global * COLS) / (ROWS_PER_GPU * COLS)  # 32768^2-equivalents per iteration
-    dev = grp.local_rank
+    dev = int(os.environ.get("BENCH_DEVICE", grp.local_rank))  # BENCH_DEVICE: ranks sharing one GPU (smoke only)
 
-    nid = None
-    if world > 1:
-        nid = D.broadcast_bytes(D.nccl_unique_id() if rank == 0 else None, src=0)
-    s = D.DistSession(rows_global, COLS, rank, world, dev, nid)
+    s = D.make_session(rows_global, COLS, dev, args.exchange)  # collective (peer handles / NCCL id)
     lay = s.layout
     rows_local = s.rows
 
@@ -313,7 +310,10 @@ def run_ours(args, grp: Group):
                         f"(fi=1/1.1), {args.steps} fused iterations",
             "rows_global": rows_global, "cols": COLS, "rows_per_gpu": rows_local, "storage": "f32",
             "arithmetic": "f64 products rounded once to f32, f64 sums (bit-compatible with the reference)",
-            "parallelism": f"row-sharded x{world}" + (", NCCL allreduce of cols+N f64 per iteration" if world > 1 else ""),
+            "parallelism": f"row-sharded x{world}" + (
+                (", column sums exchanged once per iteration inside the finalize kernels over peer memory "
+                 "(CUDA IPC, NVLink): cols+1 f64 pushed to every rank, ascending-rank sum")
+                if args.exchange == "peer" else ", NCCL allreduce of cols+N f64 per iteration") if world > 1 else ""),
             "l2": f"no flush: the resident matrix ({bytes_iter_local / 2 / 2**30:.1f} GiB/GPU) exceeds the 126 MB L2",
             "layout": {k: lay[k] for k in ("G", "groups", "slice", "threads", "nbuf", "rows_per_step", "smem_bytes")},
         },
@@ -337,6 +337,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default=os.environ.get("UOT_EXCHANGE", "peer"),
+                    help="N>1: fused peer-memory exchange (default) or one NCCL allreduce per iteration")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=8192)

@@ -81,6 +81,21 @@ UOT_API int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, 
                     int rank, int nranks, const uint8_t* nccl_id);
 UOT_API int uot_nccl_unique_id(uint8_t* out128);
 
+/* Multi-GPU session whose per-iteration allreduce of the column sums
+ * (distributed.hpp:88-94, allreduce_vectors src/allreduce.cpp:6-15) is fused
+ * into the finalize kernels over peer memory (CUDA IPC over NVLink/NVSwitch; two
+ * processes on one GPU also work): every rank pushes its column sums into all
+ * peers' receive tables and sums the nranks rows in ascending rank order —
+ * bit-identical on every rank, no NCCL. Collective protocol: create on every
+ * rank, all-gather the 64-byte uot_peer_handle of each rank (any transport),
+ * then uot_peer_connect(ctx, handles[nranks*64]) on every rank. */
+UOT_API int uot_create_peer(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device,
+                            int rank, int nranks);
+UOT_API int uot_peer_handle(const uot_ctx* ctx, uint8_t* out64);
+UOT_API int uot_peer_connect(uot_ctx* ctx, const uint8_t* handles);
+/* 0 single GPU, 1 NCCL allreduce, 2 fused peer-memory exchange. */
+UOT_API int uot_exchange_mode(const uot_ctx* ctx);
+
 UOT_API void uot_destroy(uot_ctx* ctx);
 UOT_API const char* uot_last_error(const uot_ctx* ctx);
 UOT_API int uot_get_layout(const uot_ctx* ctx, uot_layout* out);

@@ -16,10 +16,23 @@
 // summation order is fixed, so results are deterministic run to run; the
 // latency chain per thread is groups/8 loads instead of groups.
 //
-// Multi-GPU (distributed.hpp:88-100): REDUCE writes this rank's column partial
-// sum into the exchange vector (plus its alpha-error in slot cols+rank), the
-// host enqueues one ncclAllReduce(sum) on it, and BETA consumes the result.
+// Multi-GPU (distributed.hpp:88-100), one exchange of the column sums per
+// iteration, two ways (XCH):
+//   kXchNccl  stage 1 writes this rank's column sums into the allreduce vector
+//             (plus its alpha error in slot cols+rank), the host enqueues one
+//             ncclAllReduce(sum), stage 2 consumes the result.
+//   kXchPeer  the allreduce fused into the two stages over peer memory (CUDA
+//             IPC, NVLink/NVSwitch): stage 1 PUSHES this rank's column sums and
+//             alpha error into row `rank` of every peer's receive table with
+//             plain remote stores, then its last block raises a sequence flag in
+//             every peer (st.release.sys); stage 2 waits for all P flags in its
+//             own memory and sums the P rows in ascending rank order — exactly
+//             allreduce_vectors (src/allreduce.cpp:6-15), identical bits on every
+//             rank, no NCCL launch. Receive tables are double-buffered by the
+//             parity of the exchange sequence number (a rank can be at most one
+//             exchange ahead of any peer).
 #pragma once
+#include "ptx.cuh"
 #include "uot_device.cuh"
 
 namespace uotk {
@@ -28,15 +41,29 @@ constexpr int kFinThreads = 256;
 constexpr int kFinSlices = kFinThreads / 32;
 constexpr int kFinCols = 32;
 
+enum XchMode : int { kXchNone = 0, kXchNccl = 1, kXchPeer = 2 };
+
+// Per-rank peer-exchange region (identical layout on every rank):
+//   u64    flags[2][nranks]           sequence number of the last exchange seen per sender
+//   double recv[2][nranks][xlen]      row q = rank q's column sums, then its alpha error
+struct PeerRegion {
+  __host__ __device__ static size_t flag_bytes(unsigned nranks) { return (2ull * nranks * 8 + 255) / 256 * 256; }
+  static size_t bytes(unsigned nranks, unsigned xlen) {
+    return flag_bytes(nranks) + 2ull * nranks * xlen * sizeof(double);
+  }
+};
+
 struct FinalizeArgs {
   const double* partials;  // [groups][pitch]
   const double* cta_err;   // [grid][kErrSlots]
   const double* cpd;       // [cols]
   double* beta2;           // [2][pitch]
   double* col_sums;        // [cols]  carried FusedState::col_sums
-  double* xsum;            // [cols + nranks] allreduce vector (multi-GPU) or nullptr
+  double* xsum;            // [cols + nranks] allreduce vector (kXchNccl) or nullptr
+  unsigned char* const* peers;  // [nranks] peer-region base of every rank (kXchPeer; own included)
+  unsigned char* region;        // this rank's peer region (kXchPeer)
   Control* ctl;
-  unsigned int cols, pitch, groups, grid, rank, nranks;
+  unsigned int cols, pitch, groups, grid, rank, nranks, xlen;
   double fi;
 };
 
@@ -61,7 +88,14 @@ __device__ __forceinline__ double block_alpha_err(const FinalizeArgs& f, double*
   return m;
 }
 
-template <int MODE, bool REDUCE, bool BETA>
+__device__ __forceinline__ unsigned long long* peer_flags(unsigned char* base) {
+  return reinterpret_cast<unsigned long long*>(base);
+}
+__device__ __forceinline__ double* peer_recv(unsigned char* base, unsigned nranks) {
+  return reinterpret_cast<double*>(base + PeerRegion::flag_bytes(nranks));
+}
+
+template <int MODE, bool REDUCE, bool BETA, int XCH = kXchNone>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArgs f) {
   __shared__ double part[kFinSlices][kFinCols];
   __shared__ double red[kFinSlices];
@@ -71,6 +105,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
   const unsigned lane = threadIdx.x & 31, slice = threadIdx.x >> 5;
   const unsigned j = blockIdx.x * kFinCols + lane;
   const unsigned long long it = ctl->iter;  // completed before this sweep
+  const unsigned long long seq = ctl->xseq + 1;  // this exchange (kXchPeer)
+  const unsigned par = static_cast<unsigned>(seq & 1ull);
 
   double s = 0.0;  // column sum of column j (valid in warp 0)
   if (REDUCE) {
@@ -85,13 +121,56 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
     }
   }
 
-  if (REDUCE && !BETA) {  // multi-GPU stage 1: local partial sums -> exchange vector
-    if (slice == 0 && j < f.cols) f.xsum[j] = s;
-    if (blockIdx.x == 0) {  // this rank's alpha error in its own slot, zeros elsewhere
-      const double e = MODE == kFinIter ? block_alpha_err(f, red) : 0.0;
-      for (unsigned r = threadIdx.x; r < f.nranks; r += kFinThreads) f.xsum[f.cols + r] = r == f.rank ? e : 0.0;
+  if (REDUCE && !BETA) {  // multi-GPU stage 1: local partial sums -> the exchange
+    // this rank's alpha error; a degenerate row factor travels as -1 so every
+    // rank stops at the same iteration
+    double e = 0.0;
+    if (blockIdx.x == 0 && MODE == kFinIter) {
+      e = block_alpha_err(f, red);
+      if (ctl->alpha_bad) e = -1.0;
     }
+    if (XCH == kXchNccl) {
+      if (slice == 0 && j < f.cols) f.xsum[j] = s;
+      if (blockIdx.x == 0)
+        for (unsigned r = threadIdx.x; r < f.nranks; r += kFinThreads) f.xsum[f.cols + r] = r == f.rank ? e : 0.0;
+      return;
+    }
+    // kXchPeer: warp 0 (it holds the sums) pushes into row `rank` of every
+    // peer's receive table: 256-byte coalesced remote stores per peer
+    if (slice == 0 && j < f.cols)
+      for (unsigned q = 0; q < f.nranks; ++q)
+        peer_recv(f.peers[q], f.nranks)[(static_cast<size_t>(par) * f.nranks + f.rank) * f.xlen + j] = s;
+    if (blockIdx.x == 0 && threadIdx.x < f.nranks) {
+      double* row = peer_recv(f.peers[threadIdx.x], f.nranks) + (static_cast<size_t>(par) * f.nranks + f.rank) * f.xlen;
+      row[f.cols] = e;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&ctl->fin_count, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence_system();
+    if (threadIdx.x < f.nranks) st_release_sys_u64(&peer_flags(f.peers[threadIdx.x])[par * f.nranks + f.rank], seq);
+    if (threadIdx.x == 0) ctl->fin_count = 0;
     return;
+  }
+
+  if (XCH == kXchPeer && !REDUCE && MODE != kFinBetaOnly) {
+    // stage 2: wait until every rank's row of this exchange has landed here
+    if (threadIdx.x < f.nranks) {
+      const unsigned long long* flag = &peer_flags(f.region)[par * f.nranks + threadIdx.x];
+      if (ld_acquire_sys_u64(flag) != seq) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire_sys_u64(flag) != seq) {
+          if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+            atomicOr(&ctl->status, kStatusPeerTimeout);
+            ctl->done = 1;
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
   }
 
   // beta slot: seed produces beta(1); iteration t = it+1 produces beta(t+1).
@@ -101,6 +180,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
     if (j < f.cols) {
       if (MODE == kFinBetaOnly) {
         s = f.col_sums[j];
+      } else if (!REDUCE && XCH == kXchPeer) {
+        const double* recv = peer_recv(f.region, f.nranks) + static_cast<size_t>(par) * f.nranks * f.xlen;
+        s = 0.0;
+        for (unsigned q = 0; q < f.nranks; ++q) s += __ldcg(&recv[static_cast<size_t>(q) * f.xlen + j]);
       } else if (!REDUCE) {
         s = f.xsum[j];  // allreduced
       }
@@ -132,12 +215,22 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
   if (MODE == kFinIter) {
     if (REDUCE) {
       ea = block_alpha_err(f, red);
+    } else if (XCH == kXchPeer) {
+      const double* recv = peer_recv(f.region, f.nranks) + static_cast<size_t>(par) * f.nranks * f.xlen;
+      for (unsigned q = 0; q < f.nranks; ++q) {
+        const double v = __ldcg(&recv[static_cast<size_t>(q) * f.xlen + f.cols]);
+        ea = v < 0.0 || ea < 0.0 ? -1.0 : fmax(ea, v);
+      }
     } else {
-      for (unsigned r = 0; r < f.nranks; ++r) ea = fmax(ea, f.xsum[f.cols + r]);
+      for (unsigned r = 0; r < f.nranks; ++r) {
+        const double v = f.xsum[f.cols + r];
+        ea = v < 0.0 || ea < 0.0 ? -1.0 : fmax(ea, v);
+      }
     }
   }
   if (threadIdx.x != 0) return;
   ctl->fin_count = 0;
+  if (XCH != kXchNone && !REDUCE && MODE != kFinBetaOnly) ctl->xseq = seq;
   ctl->beta_bad = ctl->beta_bad_next;
   ctl->beta_bad_next = 0;
   if (MODE == kFinIter) {
@@ -145,7 +238,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
     volatile double* eb = &ctl->err_beta[t & 1ull];
     const double err = fmax(ea, *eb);
     *eb = 0.0;  // this slot next receives beta(t+2)
-    if (ctl->alpha_bad) {  // the row pass threw: iteration t did not complete
+    if (ctl->alpha_bad || ea < 0.0) {  // a row pass threw: iteration t did not complete
       ctl->status |= kStatusDegenerateAlpha;
       ctl->done = 1;
     } else {

@@ -119,6 +119,16 @@ __device__ __forceinline__ void ld_relaxed_b128(const void* p, unsigned long lon
       : "memory");
 }
 
+// system-scope release/acquire: flags in peer memory (CUDA IPC over NVLink).
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // 128-bit global store that streams past L1 and carries an L2 eviction hint.
 __device__ __forceinline__ void st_global_v4(float4* p, float4 v, uint64_t policy) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),

@@ -146,8 +146,16 @@ struct uot_ctx {
   int sms = 0;
   uint64_t rows = 0, cols = 0, row_offset = 0, global_rows = 0;
   int rank = 0, nranks = 1;
-  bool is_dist = false;  // created by uot_create_dist (CommStats are kept)
+  bool is_dist = false;  // created by uot_create_dist / uot_create_peer (CommStats are kept)
+  int xmode = kXchNone;  // how the column sums of the ranks are combined
   ncclComm_t comm = nullptr;
+  // kXchPeer: this rank's exchange region, every rank's region mapped here
+  unsigned char* region = nullptr;
+  size_t region_bytes = 0;
+  unsigned xlen = 0;
+  std::vector<unsigned char*> peer_ptrs;  // [nranks]; own entry = region
+  unsigned char** d_peers = nullptr;      // device copy of peer_ptrs
+  bool connected = false;
 
   // layout
   unsigned G = 1, slice = 0, pitch = 0, groups = 1, B = 1, buf_stride = 0, grid = 1;
@@ -319,6 +327,9 @@ FinalizeArgs fin_args(const uot_ctx* ctx) {
   f.grid = ctx->grid;
   f.rank = static_cast<unsigned>(ctx->rank);
   f.nranks = static_cast<unsigned>(ctx->nranks);
+  f.peers = ctx->d_peers;
+  f.region = ctx->region;
+  f.xlen = ctx->xlen;
   f.fi = ctx->fi;
   return f;
 }
@@ -355,20 +366,28 @@ int nccl_check(uot_ctx* ctx, ncclResult_t r, const char* what) {
   return ctx->fail(UOT_NCCL_ERROR, "%s: %s", what, nccl().GetErrorString(r));
 }
 
-// Multi-GPU tail: local reduce -> one allreduce of cols + nranks doubles -> beta.
+// Multi-GPU tail: local reduce -> one exchange of the column sums -> beta.
 template <int MODE>
 int launch_finalize_dist(uot_ctx* ctx) {
   const unsigned blocks = finalize_blocks(ctx->pitch);
   const FinalizeArgs f = fin_args(ctx);
   ctx->launches += 2;
-  finalize_kernel<MODE, true, false><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
+  if (ctx->xmode == kXchPeer) {  // the allreduce fused into both stages (finalize.cuh)
+    if (!ctx->connected) return ctx->fail(UOT_INVALID_PARAMETER, "peer session not connected (uot_peer_connect)");
+    finalize_kernel<MODE, true, false, kXchPeer><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
+    int rc = ctx->cuda(cudaGetLastError(), "finalize(push) launch");
+    if (rc) return rc;
+    finalize_kernel<MODE, false, true, kXchPeer><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
+    return ctx->cuda(cudaGetLastError(), "finalize(gather) launch");
+  }
+  finalize_kernel<MODE, true, false, kXchNccl><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
   int rc = ctx->cuda(cudaGetLastError(), "finalize(reduce) launch");
   if (rc) return rc;
   rc = nccl_check(ctx, nccl().AllReduce(ctx->xsum, ctx->xsum, ctx->cols + ctx->nranks, ncclFloat64,
                                         ncclSum, ctx->comm, ctx->stream),
                   "ncclAllReduce");
   if (rc) return rc;
-  finalize_kernel<MODE, false, true><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
+  finalize_kernel<MODE, false, true, kXchNccl><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
   return ctx->cuda(cudaGetLastError(), "finalize(beta) launch");
 }
 
@@ -387,6 +406,8 @@ int status_of(uot_ctx* ctx) {
   const int st = ctx->h_ctl->status;
   if (st & kStatusExchangeTimeout)
     return ctx->fail(UOT_CUDA_ERROR, "row-sum exchange timed out (CTAs not co-resident)");
+  if (st & kStatusPeerTimeout)
+    return ctx->fail(UOT_CUDA_ERROR, "peer exchange timed out (a rank stopped publishing its column sums)");
   if (st & (kStatusDegenerateAlpha | kStatusDegenerateBeta))
     return ctx->fail(UOT_DEGENERATE_SUM, "rescale_factor: %s",
                      (st & kStatusDegenerateAlpha) ? "a row sum is not strictly positive or its factor left the positive finite range"
@@ -469,8 +490,12 @@ int uot_nccl_unique_id(uint8_t* out128) {
   return UOT_OK;
 }
 
-int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device,
-                    int rank, int nranks, const uint8_t* nccl_id) {
+}  // extern "C"
+
+namespace {
+// Rank state shared by both exchange flavours (distributed.hpp:65-79).
+int create_rank(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device, int rank,
+                int nranks) {
   if (!out) return UOT_INVALID_PARAMETER;
   *out = nullptr;
   auto* ctx = new uot_ctx();
@@ -491,9 +516,20 @@ int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtyp
   ctx->rank = rank;
   ctx->nranks = nranks;
   ctx->is_dist = true;
-  int rc = create_common(ctx, device);
+  return create_common(ctx, device);
+}
+}  // namespace
+
+extern "C" {
+
+int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device,
+                    int rank, int nranks, const uint8_t* nccl_id) {
+  int rc = create_rank(out, global_rows, cols, dtype, device, rank, nranks);
   if (rc) return rc;
+  uot_ctx* ctx = *out;
   if (nranks > 1) {
+    ctx->xmode = kXchNccl;
+    if (!nccl_id) return ctx->fail(UOT_INVALID_PARAMETER, "a multi-rank session needs the NCCL id of rank 0");
     if (!nccl().ok) return ctx->fail(UOT_NCCL_ERROR, "%s", nccl().err.c_str());
     ncclUniqueId id;
     std::memcpy(id.internal, nccl_id, 128);
@@ -503,6 +539,62 @@ int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtyp
   return UOT_OK;
 }
 
+int uot_create_peer(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device, int rank,
+                    int nranks) {
+  int rc = create_rank(out, global_rows, cols, dtype, device, rank, nranks);
+  if (rc) return rc;
+  uot_ctx* ctx = *out;
+  if (nranks > 1) {
+    ctx->xmode = kXchPeer;
+    ctx->xlen = round_up(static_cast<unsigned>(ctx->cols) + 1, 32);
+    ctx->region_bytes = PeerRegion::bytes(nranks, ctx->xlen);
+    // cudaMalloc'd so the allocation can be exported with cudaIpcGetMemHandle
+    CK(cudaMalloc(reinterpret_cast<void**>(&ctx->region), ctx->region_bytes));
+    CK(cudaMemset(ctx->region, 0, ctx->region_bytes));  // flags start at 0; sequence numbers at 1
+    CK(cudaMalloc(reinterpret_cast<void**>(&ctx->d_peers), sizeof(unsigned char*) * nranks));
+  }
+  return UOT_OK;
+}
+
+int uot_peer_handle(const uot_ctx* cctx, uint8_t* out64) {
+  auto* ctx = const_cast<uot_ctx*>(cctx);
+  if (!ctx || !out64) return UOT_INVALID_PARAMETER;
+  if (ctx->xmode != kXchPeer) return ctx->fail(UOT_INVALID_PARAMETER, "not a multi-rank peer session");
+  CK(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  CK(cudaIpcGetMemHandle(&h, ctx->region));
+  std::memcpy(out64, &h, 64);
+  return UOT_OK;
+}
+
+int uot_peer_connect(uot_ctx* ctx, const uint8_t* handles) {
+  if (!ctx || !handles) return UOT_INVALID_PARAMETER;
+  if (ctx->xmode != kXchPeer) return ctx->fail(UOT_INVALID_PARAMETER, "not a multi-rank peer session");
+  if (ctx->connected) return ctx->fail(UOT_INVALID_PARAMETER, "peer session already connected");
+  CK(cudaSetDevice(ctx->device));
+  ctx->peer_ptrs.assign(ctx->nranks, nullptr);
+  for (int q = 0; q < ctx->nranks; ++q) {
+    if (q == ctx->rank) {
+      ctx->peer_ptrs[q] = ctx->region;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + 64 * static_cast<size_t>(q), 64);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return ctx->fail(UOT_CUDA_ERROR, "cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
+    ctx->peer_ptrs[q] = static_cast<unsigned char*>(p);
+  }
+  CK(cudaMemcpy(ctx->d_peers, ctx->peer_ptrs.data(), sizeof(unsigned char*) * ctx->nranks,
+                cudaMemcpyHostToDevice));
+  ctx->connected = true;
+  return UOT_OK;
+}
+
+int uot_exchange_mode(const uot_ctx* ctx) { return ctx ? ctx->xmode : -1; }
+
 void uot_destroy(uot_ctx* ctx) {
   if (!ctx) return;
   if (ctx->stream) {
@@ -510,6 +602,10 @@ void uot_destroy(uot_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
   }
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
+  for (int q = 0; q < static_cast<int>(ctx->peer_ptrs.size()); ++q)
+    if (q != ctx->rank && ctx->peer_ptrs[q]) cudaIpcCloseMemHandle(ctx->peer_ptrs[q]);
+  if (ctx->region) cudaFree(ctx->region);
+  if (ctx->d_peers) cudaFree(ctx->d_peers);
   for (auto e : ctx->ev) cudaEventDestroy(e);
   void* bufs[] = {ctx->P,     ctx->rpd,   ctx->cpd,      ctx->alpha,   ctx->beta2, ctx->col_sums, ctx->xsum,
                   ctx->partials, ctx->cta_err, ctx->xrec, ctx->ctl, ctx->dflag};

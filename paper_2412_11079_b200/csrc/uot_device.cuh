@@ -8,6 +8,8 @@ namespace uotk {
 constexpr int kStatusDegenerateAlpha = 1;   // rescale_factor threw for a row (scaling.cpp:15-22)
 constexpr int kStatusDegenerateBeta = 2;    // beta_from_state threw (fused.hpp:146-157)
 constexpr int kStatusExchangeTimeout = 4;   // a peer CTA never published (co-residency bug)
+constexpr int kStatusPeerTimeout = 8;       // a peer rank never published its column sums
+constexpr unsigned long long kPeerTimeoutNs = 60000000000ull;
 constexpr int kErrSlots = 4;                // max|alpha-1| slots per sweep CTA (one per factor warp)
 constexpr unsigned long long kExchangeTimeoutNs = 4000000000ull;
 
@@ -19,6 +21,7 @@ constexpr unsigned long long kExchangeTimeoutNs = 4000000000ull;
 struct Control {
   unsigned long long iter;    // completed iterations since the problem was set
   unsigned long long epoch;   // never reset: tags of the cross-CTA exchange
+  unsigned long long xseq;    // never reset: completed cross-rank exchanges (peer flags)
   unsigned long long allreduce_calls;   // CommStats (distributed.hpp:24-27)
   unsigned long long doubles_reduced;
   double tol;

@@ -6,17 +6,19 @@ driving its own B200:
 
 * rows are split by RankPartition::make(P, rows) (src/plan.cpp:35-44) — rank r
   keeps its contiguous row block resident in HBM;
-* every iteration ends with ONE sum-allreduce of a (cols + P)-vector of f64 over
-  NCCL (NVLink/NVSwitch): the rank's column partials (distributed.hpp:88-94) plus
-  one slot per rank carrying its max|alpha-1| so every rank derives the same
-  convergence error (the "scalar max-reduction" the reference comment at
-  distributed.hpp:50-51 anticipates, folded into the same call);
+* every iteration ends with ONE exchange of the ranks' column partials
+  (distributed.hpp:88-94) plus each rank's max|alpha-1| (the "scalar
+  max-reduction" the reference comment at distributed.hpp:50-51 anticipates,
+  folded into the same exchange), either fused into the finalize kernels over
+  peer memory (default: CUDA IPC over NVLink/NVSwitch, ascending-rank sum =
+  allreduce_vectors, src/allreduce.cpp:6-15) or as one ncclAllReduce;
 * every rank then derives the identical beta from the identical reduced vector
   (distributed.hpp:96-100).
 
-The NCCL communicator lives inside the C++ session (include/uot_cuda.h,
-uot_create_dist); torch.distributed (any backend, gloo is enough) only carries
-the 128-byte NCCL id from rank 0 and the host-side barriers.
+The peer mappings / NCCL communicator live inside the C++ session
+(include/uot_cuda.h, uot_create_peer / uot_create_dist); torch.distributed (any
+backend, gloo is enough) only carries the 64-byte IPC handles (or the 128-byte
+NCCL id of rank 0) and the host-side barriers.
 """
 from __future__ import annotations
 
@@ -82,32 +84,77 @@ def rank_block(ranks: int, rows: int, rank: int):
 
 class DistSession(uot.Session):
     """Session for rank `rank` of `nranks` over `global_rows` rows. With
-    nranks == 1 it is an ordinary single-GPU session (no NCCL)."""
+    nranks == 1 it is an ordinary single-GPU session (no exchange).
+
+    exchange="peer" (default): the per-iteration allreduce is fused into the
+    finalize kernels over peer memory (CUDA IPC over NVLink/NVSwitch; see
+    csrc/finalize.cuh) — call connect() with every rank's handle() before use.
+    exchange="nccl": one ncclAllReduce per iteration (needs the NCCL id of rank 0).
+    """
 
     def __init__(self, global_rows: int, cols: int, rank: int, nranks: int, device: int,
-                 nccl_id: bytes | None = None):
-        if nranks > 1 and nccl_id is None:
-            raise uot.InvalidParameter("a multi-rank session needs the NCCL id of rank 0")
-        super().__init__(global_rows, cols, device, dist=(rank, nranks, nccl_id or b"\0" * 128))
-        self.rank, self.nranks = rank, nranks
+                 nccl_id: bytes | None = None, exchange: str = "peer"):
+        if exchange not in ("peer", "nccl"):
+            raise uot.InvalidParameter(f"exchange must be 'peer' or 'nccl', not {exchange!r}")
+        if exchange == "nccl" and nranks > 1 and nccl_id is None:
+            raise uot.InvalidParameter("a multi-rank NCCL session needs the NCCL id of rank 0")
+        dist = (rank, nranks, "peer") if exchange == "peer" else (rank, nranks, nccl_id or b"\0" * 128)
+        super().__init__(global_rows, cols, device, dist=dist)
+        self.rank, self.nranks, self.exchange = rank, nranks, exchange
+
+    def handle(self) -> bytes:
+        """The 64-byte CUDA IPC handle of this rank's exchange region."""
+        buf = (C.c_uint8 * 64)()
+        self._check(uot.lib().uot_peer_handle(self._h, C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
+    def connect(self, handles: list[bytes]):
+        """Map every rank's exchange region (handles in rank order; own included)."""
+        if len(handles) != self.nranks or any(len(h) != 64 for h in handles):
+            raise uot.InvalidParameter(f"connect needs {self.nranks} handles of 64 bytes")
+        buf = (C.c_uint8 * (64 * self.nranks)).from_buffer_copy(b"".join(handles))
+        self._check(uot.lib().uot_peer_connect(self._h, C.cast(buf, C.c_void_p)))
+
+    def exchange_mode(self) -> int:
+        return int(uot.lib().uot_exchange_mode(self._h))
 
 
-def make_session(global_rows: int, cols: int, device: int | None = None) -> DistSession:
-    """Collective: one DistSession per rank of the current torch process group."""
+def all_gather_bytes(data: bytes) -> list[bytes]:
+    """Every rank's byte string, in rank order, over the torch process group."""
+    dist = _torch_dist()
+    if dist is None:
+        return [data]
+    out: list = [None] * dist.get_world_size()
+    dist.all_gather_object(out, data)
+    return out
+
+
+def make_session(global_rows: int, cols: int, device: int | None = None,
+                 exchange: str | None = None) -> DistSession:
+    """Collective: one DistSession per rank of the current torch process group.
+    The exchange defaults to $UOT_EXCHANGE or "peer"."""
     dist = _torch_dist()
     rank = dist.get_rank() if dist else 0
     world = dist.get_world_size() if dist else 1
     if device is None:
         device = int(os.environ.get("LOCAL_RANK", rank))
+    exchange = exchange or os.environ.get("UOT_EXCHANGE", "peer")
     nid = None
-    if world > 1:
+    if world > 1 and exchange == "nccl":
         nid = broadcast_bytes(nccl_unique_id() if rank == 0 else None, src=0)
-    return DistSession(global_rows, cols, rank, world, device, nid)
+    s = DistSession(global_rows, cols, rank, world, device, nid, exchange)
+    if world > 1 and exchange == "peer":
+        try:
+            s.connect(all_gather_bytes(s.handle()))
+        except BaseException:
+            s.close()
+            raise
+    return s
 
 
 def distributed_solve(p: uot.Problem, tol: float, max_iter: int, device: int | None = None,
-                      session: DistSession | None = None, global_rows: int | None = None
-                      ) -> DistributedResult:
+                      session: DistSession | None = None, global_rows: int | None = None,
+                      exchange: str | None = None) -> DistributedResult:
     """distributed_solve (distributed.hpp:52-130) across the ranks of the current
     torch process group (world size 1 without one).
 
@@ -118,7 +165,7 @@ def distributed_solve(p: uot.Problem, tol: float, max_iter: int, device: int | N
     t0 = time.perf_counter()
     grows = global_rows if global_rows is not None else p.m()
     own = session is None
-    s = make_session(grows, p.n(), device) if own else session
+    s = make_session(grows, p.n(), device, exchange) if own else session
     try:
         b, e = s.row_offset, s.row_offset + s.rows
         if global_rows is None:

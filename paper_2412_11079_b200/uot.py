@@ -109,6 +109,10 @@ def lib():
     L.uot_create.argtypes = [C.POINTER(_P), _u64, _u64, _i, _i]
     L.uot_create_dist.argtypes = [C.POINTER(_P), _u64, _u64, _i, _i, _i, _i, _P]
     L.uot_nccl_unique_id.argtypes = [_P]
+    L.uot_create_peer.argtypes = [C.POINTER(_P), _u64, _u64, _i, _i, _i, _i]
+    L.uot_peer_handle.argtypes = [_P, _P]
+    L.uot_peer_connect.argtypes = [_P, _P]
+    L.uot_exchange_mode.argtypes = [_P]
     L.uot_destroy.argtypes = [_P]
     L.uot_destroy.restype = None
     L.uot_last_error.argtypes = [_P]
@@ -307,6 +311,10 @@ class Session:
         L = lib()
         if dist is None:
             rc = L.uot_create(C.byref(self._h), int(rows), int(cols), UOT_F32, int(device))
+        elif dist[2] == "peer":  # (rank, nranks, "peer"): connect() with every rank's handle next
+            rank, nranks, _ = dist
+            rc = L.uot_create_peer(C.byref(self._h), int(rows), int(cols), UOT_F32, int(device),
+                                   int(rank), int(nranks))
         else:
             rank, nranks, nccl_id = dist
             idbuf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id).ljust(128, b"\0"))
