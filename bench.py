@@ -300,6 +300,9 @@ def run_ours(args, grp: Group):
 
     if rank != 0:
         return None
+    xdesc = (", column sums exchanged once per iteration inside the finalize kernels over peer memory "
+             "(CUDA IPC, NVLink): cols+1 f64 pushed to every rank, ascending-rank sum") \
+        if args.exchange == "peer" else ", NCCL allreduce of cols+N f64 per iteration"
     return {
         "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
@@ -310,10 +313,7 @@ def run_ours(args, grp: Group):
                         f"(fi=1/1.1), {args.steps} fused iterations",
             "rows_global": rows_global, "cols": COLS, "rows_per_gpu": rows_local, "storage": "f32",
             "arithmetic": "f64 products rounded once to f32, f64 sums (bit-compatible with the reference)",
-            "parallelism": f"row-sharded x{world}" + (
-                (", column sums exchanged once per iteration inside the finalize kernels over peer memory "
-                 "(CUDA IPC, NVLink): cols+1 f64 pushed to every rank, ascending-rank sum")
-                if args.exchange == "peer" else ", NCCL allreduce of cols+N f64 per iteration") if world > 1 else ""),
+            "parallelism": f"row-sharded x{world}" + (xdesc if world > 1 else ""),
             "l2": f"no flush: the resident matrix ({bytes_iter_local / 2 / 2**30:.1f} GiB/GPU) exceeds the 126 MB L2",
             "layout": {k: lay[k] for k in ("G", "groups", "slice", "threads", "nbuf", "rows_per_step", "smem_bytes")},
         },
