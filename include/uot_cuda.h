@@ -64,6 +64,8 @@ typedef struct uot_layout {
   uint32_t nbuf;         /* shared-memory ring slots */
   uint32_t sms;
   int32_t rank, nranks, device, evict_first;
+  int32_t smid_map;      /* sweep CTAs addressed by SM id (row groups on neighbouring SMs) */
+  int32_t exchange;      /* 0 single GPU, 1 NCCL allreduce, 2 fused peer-memory exchange */
 } uot_layout;
 
 /* ---- sessions ---------------------------------------------------------- */

@@ -61,6 +61,7 @@ struct SweepArgs {
   unsigned int B;             // rows per pipeline batch (<= BM; 1 when G > 1)
   unsigned int buf_stride;    // bytes per smem ring slot (128-aligned, >= B*slice*4)
   int evict_first;            // stream P past L2 (problem larger than L2)
+  int smid_map;               // CTA slot = %smid (the grid covers every SM exactly once)
   double fi;
 };
 
@@ -325,7 +326,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned G = a.G;
-  const unsigned group = blockIdx.x / G, g = blockIdx.x % G;
+  // CTA slot: blockIdx, or (smid_map) the SM id, so the G CTAs of a row group
+  // sit on neighbouring SMs (same TPC pair / GPC, same die).
+  const unsigned cta = a.smid_map ? smid() : blockIdx.x;
+  const unsigned group = cta / G, g = cta % G;
   // balanced_blocks over groups (plan.cpp:11-21): first rows%groups get one more.
   const unsigned long long base = a.rows / a.groups, rem = a.rows % a.groups;
   const unsigned long long r0 = group * base + (group < rem ? group : rem);
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         ulonglong2* const xmine = xrow + g;
         const ulonglong2* const xpeer = xrow + lane;
 #else
-        ulonglong2* const xmine = &a.xrec[static_cast<size_t>(blockIdx.x) * kRing + (s % kRing)];
+        ulonglong2* const xmine = &a.xrec[static_cast<size_t>(cta) * kRing + (s % kRing)];
         const ulonglong2* const xpeer = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (s % kRing)];
 #endif
         if (lane == 0)
@@ -524,9 +528,9 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     }
     for (int o = 16; o > 0; o >>= 1) errmax = fmax(errmax, __shfl_xor_sync(0xffffffffu, errmax, o));
     if (lane == 0) {
-      a.cta_err[kErrSlots * blockIdx.x + f] = errmax;
+      a.cta_err[kErrSlots * cta + f] = errmax;
       if (f == 0)
-        for (int k = NF; k < kErrSlots; ++k) a.cta_err[kErrSlots * blockIdx.x + k] = 0.0;
+        for (int k = NF; k < kErrSlots; ++k) a.cta_err[kErrSlots * cta + k] = 0.0;
     }
 #ifdef UOT_TRACE
     tr_acc[9] = clock64() - tr_f0;

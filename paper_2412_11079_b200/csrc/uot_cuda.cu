@@ -127,6 +127,14 @@ NcclApi& nccl() {
 
 unsigned round_up(unsigned x, unsigned m) { return (x + m - 1) / m * m; }
 
+__global__ void smid_probe_kernel(unsigned* out) {
+  extern __shared__ unsigned char probe_smem[];
+  if (threadIdx.x == 0) {
+    probe_smem[0] = 0;
+    out[blockIdx.x] = uotk::smid();
+  }
+}
+
 void balanced_bounds(uint64_t k, uint64_t rows, uint64_t* bounds) {  // plan.cpp:11-21
   const uint64_t base = rows / k, rem = rows % k;
   bounds[0] = 0;
@@ -163,6 +171,7 @@ struct uot_ctx {
   const SweepCfg* cfg = nullptr;
   int evict_first = 0;
   int full = 0;
+  int smid_map = 0;
 
   // device buffers
   float* P = nullptr;
@@ -207,6 +216,33 @@ struct uot_ctx {
 
 namespace {
 
+// G > 1 and one sweep CTA on every SM: address CTAs by %smid so the G CTAs of a
+// row group run on neighbouring SMs. Enabled only when a probe launch with the
+// sweep's footprint shows %smid is a permutation of [0, grid) (UOT_SMID_MAP=0 off).
+int probe_smid_map(uot_ctx* ctx) {
+  ctx->smid_map = 0;
+  int nsm = 0;
+  if (ctx->cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device), "attr")) return UOT_CUDA_ERROR;
+  if (ctx->G < 2 || static_cast<int>(ctx->grid) != nsm || !env_int("UOT_SMID_MAP", 1)) return UOT_OK;
+  unsigned* d = nullptr;
+  CK(cudaMalloc(&d, ctx->grid * sizeof(unsigned)));
+  CK(cudaFuncSetAttribute(smid_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem)));
+  smid_probe_kernel<<<ctx->grid, 32, ctx->smem, ctx->stream>>>(d);
+  std::vector<unsigned> h(ctx->grid);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, ctx->grid * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d);
+  CK(e);
+  std::vector<char> seen(ctx->grid, 0);
+  for (unsigned v : h) {
+    if (v >= ctx->grid || seen[v]) return UOT_OK;
+    seen[v] = 1;
+  }
+  ctx->smid_map = 1;
+  return UOT_OK;
+}
+
 int plan_layout(uot_ctx* ctx) {
   const uint64_t cols = ctx->cols;
   if (cols > (1ull << 26)) return ctx->fail(UOT_CONFIG_ERROR, "cols %llu too large", (unsigned long long)cols);
@@ -234,6 +270,8 @@ int plan_layout(uot_ctx* ctx) {
   ctx->smem = cfg->smem_bytes(ctx->buf_stride);
   ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * 4 > (64ull << 20) ? 1 : 0;
   ctx->full = slice == static_cast<unsigned>(4 * cfg->nt * cfg->v) ? 1 : 0;
+  int rc = probe_smid_map(ctx);
+  if (rc) return rc;
   for (SweepFn fn : {cfg->iter[ctx->full], cfg->seed[ctx->full]}) {
     if (!fn) continue;
     const int rc = ctx->cuda(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
@@ -308,6 +346,7 @@ SweepArgs sweep_args(const uot_ctx* ctx) {
   a.B = ctx->B;
   a.buf_stride = ctx->buf_stride;
   a.evict_first = ctx->evict_first;
+  a.smid_map = ctx->smid_map;
   a.fi = ctx->fi;
   return a;
 }
@@ -638,6 +677,8 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->nranks = ctx->nranks;
   o->device = ctx->device;
   o->evict_first = ctx->evict_first;
+  o->smid_map = ctx->smid_map;
+  o->exchange = ctx->xmode;
   return UOT_OK;
 }
 
