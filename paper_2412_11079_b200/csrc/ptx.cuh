@@ -40,9 +40,31 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase
+// completes (or the hint expires) instead of re-issuing the probe — spinning
+// waiters otherwise take issue slots from the compute warps of the same SMSP.
+#ifndef UOT_MBAR_SUSPEND_NS
+#define UOT_MBAR_SUSPEND_NS 0x989680
+#endif
+__device__ __forceinline__ bool mbar_try_wait_suspend(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "n"(UOT_MBAR_SUSPEND_NS)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if UOT_MBAR_SUSPEND_NS > 0
+  while (!mbar_try_wait_suspend(bar, parity)) {
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // ------------------------------------------------------- 1-D bulk copies --

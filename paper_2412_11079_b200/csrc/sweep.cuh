@@ -8,34 +8,32 @@
 //   init_col_sums (the seed)  include/uot/fused.hpp:96-110
 //   ordered partial reduction include/uot/fused.hpp:242-248 -> finalize.cuh
 //
-// B200 design (DESIGN.md §3):
+// B200 design (DESIGN.md §4):
 //   * P is row-major [rows][pitch] fp32 in HBM; each row is cut into G column
 //     slices of `slice` floats (G = ceil(cols/8192)). A "group" of G CTAs owns a
 //     contiguous, balanced block of rows (plan.cpp:11-21 rule); CTA g of the
 //     group owns slice g of every row in the block. grid = groups * G <= #SMs,
 //     one CTA per SM, persistent over the block.
-//   * Warp-specialised: NW compute warps + 1 control warp. The control warp
-//     streams rows through a ring of NBUF shared-memory slots with 1-D bulk
-//     copies (TMA engine, UBLKCP) signalled on mbarriers, L batches ahead,
-//     derives the row factors, and stores finished rows back with bulk
-//     shared->global copies. Both sweeps run out of shared memory in place, so
-//     P is read from and written to HBM exactly once per iteration.
-//   * Compute warps never meet a CTA-wide barrier: they hand batches to the
-//     control warp through mbarriers (done1: row partials written; done2: sweep
-//     2 finished) and wait only for the data (full) and the factors (alpha_rdy),
-//     which the control warp produces one batch ahead of need.
+//   * Warp roles. A producer warp streams batches (B rows of the CTA's slice)
+//     through a ring of NBUF shared-memory slots with 1-D bulk copies (TMA
+//     engine, UBLKCP) signalled on mbarriers and bulk-stores finished batches
+//     back. Both sweeps run in place in shared memory, so P is read from and
+//     written to HBM exactly once per iteration. NF factor warps turn row sums
+//     into row factors. NW compute warps do the arithmetic.
+//   * Compute warps never meet a CTA-wide barrier: they wait only for data
+//     (full) and factors (alpha_rdy) and hand work on through mbarriers (done1:
+//     row partials written; done2: sweep 2 finished). Step s runs sweep 1 of
+//     batch s, then sweep 2 of batch s-LA-1, then the row reduction of batch s.
 //   * Per-column state lives in registers of the owning thread: beta_j (f64)
 //     and the column partial next_j (f64). Thread t owns float4 chunks
 //     t, t+NT, ... of the slice (conflict-free 128-bit smem access).
-//   * Row sums: thread partial -> warp xor-tree -> per-warp smem -> control
-//     lane sums the NW warp partials in warp order. With G > 1 the G CTA
-//     partials of a row are exchanged through L2 as 128-bit single-copy-atomic
-//     {value, tag} records (no fences) with an LA-batch lag that hides the
-//     round trip, then summed in ascending g, so every CTA of the group derives
-//     the bit-identical alpha_i. No float atomics; deterministic run to run.
+//   * Row sums: thread partial -> warp xor-tree -> per-warp smem -> factor lane
+//     sums the NW warp partials in warp order. With G > 1 the G CTA partials of
+//     a row are exchanged through L2 as 128-bit single-copy-atomic {value, tag}
+//     records (no fences), summed in ascending g, so every CTA of the group
+//     derives the bit-identical alpha_i. No float atomics: deterministic.
 //   * Arithmetic is exactly the reference's: f64 products rounded once to fp32
-//     (F2F.F32.F64), f64 sums of the stored fp32 values. f32->f64 uses a
-//     two-integer-op conversion with an exact out-of-line fallback.
+//     (F2F.F32.F64), f64 sums of the stored fp32 values (see ScreenBounds).
 #pragma once
 #include <cstdint>
 
@@ -65,15 +63,25 @@ struct SweepArgs {
   double fi;
 };
 
-// Optional phase timers (build with -DUOT_TRACE): clock64 cycles per phase,
-// summed over CTAs into uot_trace[]; read back with uot_trace_read().
+// Optional wait timers (build with -DUOT_TRACE): clock64 cycles spent in the
+// waits only (6 registers, so the build runs at close to full speed), summed
+// over CTAs into uot_trace[] and read back with uot_trace_read(): 0 factor wait
+// done1, 2 exchange poll, 3 pow+arrive, 4 producer wait done2, 16 compute wait
+// full, 19 compute wait alpha; 8/9/21 role totals.
 #ifdef UOT_TRACE
 __device__ unsigned long long uot_trace[32];
-#define TR_DECL unsigned long long tr_t0 = 0, tr_acc[32] = {0}; (void)tr_t0;
+__host__ __device__ constexpr int tr_slot(int id) {
+  return id == 0 ? 0 : id == 2 ? 1 : id == 3 ? 2 : id == 4 ? 3 : id == 16 ? 4 : id == 19 ? 5 : -1;
+}
+#define TR_DECL unsigned long long tr_t0 = 0, tr_acc[6] = {0, 0, 0, 0, 0, 0}; (void)tr_t0;
 #define TR_BEGIN() tr_t0 = clock64()
-#define TR_END(id) tr_acc[id] += clock64() - tr_t0
-#define TR_FLUSH(lo, hi)                                                   \
-  for (int i_ = lo; i_ < hi; ++i_) atomicAdd(&uot_trace[i_], tr_acc[i_])
+#define TR_END(id)                                                  \
+  do {                                                              \
+    if (tr_slot(id) >= 0) tr_acc[tr_slot(id)] += clock64() - tr_t0; \
+  } while (0)
+#define TR_FLUSH(lo, hi)           \
+  for (int i_ = lo; i_ < hi; ++i_) \
+    if (tr_slot(i_) >= 0) atomicAdd(&uot_trace[i_], tr_acc[tr_slot(i_) < 0 ? 0 : tr_slot(i_)])
 #else
 #define TR_DECL
 #define TR_BEGIN()
@@ -90,16 +98,19 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;  // xor tree: every lane holds the bit-identical total (fp add commutes)
 }
 
-
 // ------------------------------------------------------ per-row sweep bodies --
 // A thread owns float4 chunks q = tid + k*NT (k < V) of the slice. FULL: every
 // chunk exists (slice == 4*NT*V); otherwise missing chunks carry 1.0f through
 // the arithmetic and are never stored or summed.
 //
-// Exactness: f32 -> f64 is two integer ops (fastd) for positive normal floats.
-// Each group of values is screened with one VIADDMNMX per value (nn_max) and
-// routed to hardware conversions if anything is zero/subnormal/inf/nan, so the
-// result equals the reference's double(x) for every input.
+// Exactness. f32 -> f64 is two integer ops (fastd) for positive normal floats
+// (hardware F2F.F64.F32 runs on the 16/clk/SM conversion pipe, which caps the
+// sweep near the HBM rate: profiles/r01_conv_microbench.txt). Each group of x0
+// values is screened with one VIADDMNMX per value against a per-thread window
+// (ScreenBounds) that certifies x0 AND x1 = f32(f64(x0)*beta_j) positive normal;
+// otherwise the group takes exact hardware conversions. The column sums widen
+// x2 with the exact hardware conversion (no screen: the next iteration screens
+// x2 as its x0). f64 -> f32 is one F2F.F32.F64 (RN), the reference's T(double).
 
 __device__ __forceinline__ uint32_t nn_max(uint32_t m, float x) {
   return max(m, __float_as_uint(x) - 0x800000u);  // >= 0x7f000000 <=> not positive normal
@@ -115,132 +126,156 @@ __device__ __forceinline__ float& comp(float4& v, int e) {
 
 // Chunks are processed in groups of KG float4 (8 values for KG = 2): one screen
 // and one branch per group keeps the fast path branch-light while bounding the
-// live registers (V = 4 would otherwise spill under the 96-register cap of a
-// 19-warp CTA).
+// live registers under the 96-register cap of a 19-warp CTA.
 template <int V>
 struct ChunkGroup {
   static constexpr int KG = (V <= 2 || V % 2 != 0) ? V : 2;
-  static constexpr int NG = V / KG;
   static_assert(V % KG == 0, "V must be a multiple of the chunk group");
 };
 
-// fused.hpp:125-131 for this thread's part of one row: x <- f32(f64(x)*beta_j),
-// returns the f64 sum of the stored values; `x1bad` when a stored value is not
-// positive normal (sweep 2 then converts this row exactly).
+// Screen window of a thread: x0 passes iff lo <= x0 <= hi as floats, with
+// lo = max(FLT_MIN, FLT_MIN/beta_min), hi = min(FLT_MAX, FLT_MAX/beta_max)
+// rounded inward over the thread's beta_j: then x0*beta_j lies in
+// [FLT_MIN, FLT_MAX] exactly, so both rounding steps keep x1 positive normal.
+struct ScreenBounds {
+  uint32_t lo, span;  // bits(lo), bits(hi) - bits(lo)
+};
+__device__ __forceinline__ ScreenBounds screen_bounds(const double* beta, int n) {
+  // padding columns carry beta = 0 and x = 0: they fail any window, so skip them
+  double bmin = 1e308, bmax = 0.0;
+#pragma unroll
+  for (int i = 0; i < n; ++i) {
+    if (beta[i] > 0.0) {
+      bmin = fmin(bmin, beta[i]);
+      bmax = fmax(bmax, beta[i]);
+    }
+  }
+  if (!(bmax > 0.0)) bmin = bmax = 1.0;
+  const double tiny = 1.1754943508222875e-38, big = 3.4028234663852886e38;  // FLT_MIN, FLT_MAX
+  const float lo = __double2float_ru(fmax(tiny, tiny / bmin * (1.0 + 0x1p-40)));
+  const float hi = __double2float_rd(fmin(big, big / bmax * (1.0 - 0x1p-40)));
+  ScreenBounds b;
+  b.lo = __float_as_uint(lo);
+  b.span = (bmax < 1e300 && lo <= hi) ? __float_as_uint(hi) - __float_as_uint(lo) : 0u;
+  if (b.span == 0u) b.lo = 0xffffffffu;  // empty window: every group takes the exact path
+  return b;
+}
+__device__ __forceinline__ uint32_t sc_max(uint32_t m, float x, uint32_t lo) {
+  return max(m, __float_as_uint(x) - lo);  // wraps for x < lo: fails the window test
+}
+
+// Sweep 1 of one chunk group (fused.hpp:125-131): x <- f32(f64(x)*beta_j) in
+// place, t[e] = sum of f64(x); `bad` when the group took the exact path.
+template <int NT, int KG, bool FULL>
+__device__ __forceinline__ void group_sweep1(float4* row, float4 (&v)[KG], uint32_t m, int g0, unsigned tid,
+                                             unsigned nq, const double* beta, ScreenBounds sb, double (&t)[4],
+                                             bool& bad) {
+  if (m <= sb.span) {  // x0 and x1 certified positive normal: two-op widening both times
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(fastd(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) t[e] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk)
+      if (FULL || tid + (g0 + kk) * NT < nq)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t[e] += fastd(comp(v[kk], e));
+  } else {  // exact hardware conversions for any input
+    bad = true;
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        comp(v[kk], e) = d2f(static_cast<double>(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) t[e] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk)
+      if (FULL || tid + (g0 + kk) * NT < nq)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t[e] += static_cast<double>(comp(v[kk], e));
+  }
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk) {
+    const unsigned q = tid + (g0 + kk) * NT;
+    if (FULL || q < nq) row[q] = v[kk];
+  }
+}
+
+// Sweep 2 of one chunk group (fused.hpp:135-142): x <- f32(f64(x)*alpha) in
+// place, next_j += f64(x). EXACT: x1 may be non-normal (hardware widening).
+template <int NT, int KG, bool FULL, bool EXACT>
+__device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g0, unsigned tid, unsigned nq,
+                                             double al, double* acc) {
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      comp(w[kk], e) = d2f((EXACT ? static_cast<double>(comp(w[kk], e)) : fastd(comp(w[kk], e))) * al);
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk) {
+    const unsigned q = tid + (g0 + kk) * NT;
+    if (FULL || q < nq) {
+      row[q] = w[kk];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(w[kk], e));
+    }
+  }
+}
+
+template <int NT, int KG, bool FULL>
+__device__ __forceinline__ void load_group(const float4* row, float4 (&v)[KG], int g0, unsigned tid, unsigned nq) {
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk) {
+    const unsigned q = tid + (g0 + kk) * NT;
+    v[kk] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
+  }
+}
+
+template <int KG>
+__device__ __forceinline__ uint32_t screen_group(float4 (&v)[KG], uint32_t lo) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m = sc_max(m, comp(v[kk], e), lo);
+  return m;
+}
+
+// Sweep 1 of this thread's part of one row; returns the f64 row partial.
 template <int NT, int V, bool FULL>
 __device__ __forceinline__ double row_sweep1(float4* row, unsigned tid, unsigned nq, const double* beta,
-                                             bool& x1bad) {
+                                             ScreenBounds sb, bool& bad) {
   constexpr int KG = ChunkGroup<V>::KG;
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  double s[4];
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
     float4 v[KG];
-    uint32_t m = 0;
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      const unsigned q = tid + (g0 + kk) * NT;
-      v[kk] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[kk], e));
-    }
-    if (nn_ok(m)) {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(fastd(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          comp(v[kk], e) = d2f(static_cast<double>(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
-    }
-    uint32_t m1 = 0;
+    load_group<NT, KG, FULL>(row, v, g0, tid, nq);
+    const uint32_t m = screen_group<KG>(v, sb.lo);
     double t[4];
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      const unsigned q = tid + (g0 + kk) * NT;
-      if (FULL || q < nq) {
-        row[q] = v[kk];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          m1 = nn_max(m1, comp(v[kk], e));
-          const double x = fastd(comp(v[kk], e));
-          t[e] = kk == 0 ? x : t[e] + x;
-        }
-      } else if (kk == 0) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) t[e] = 0.0;
-      }
-    }
-    if (!nn_ok(m1)) {
-      x1bad = true;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) t[e] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-        if (FULL || tid + (g0 + kk) * NT < nq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) t[e] += static_cast<double>(comp(v[kk], e));
-    }
+    group_sweep1<NT, KG, FULL>(row, v, m, g0, tid, nq, beta, sb, t, bad);
 #pragma unroll
     for (int e = 0; e < 4; ++e) s[e] = g0 == 0 ? t[e] : s[e] + t[e];
   }
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
-// fused.hpp:135-142 for this thread's part of one row: x <- f32(f64(x)*alpha),
-// next_j += f64(x). The result goes back to the smem slot (bulk-stored by the
-// producer) or, with `grow`, straight to HBM with 128-bit streaming stores.
+// Sweep 2 of this thread's part of one row.
 template <int NT, int V, bool FULL>
-__device__ __forceinline__ void row_sweep2(float4* row, float4* grow, uint64_t pol, unsigned tid, unsigned nq,
-                                           double al, bool x1bad, double* acc) {
+__device__ __forceinline__ void row_sweep2(float4* row, unsigned tid, unsigned nq, double al, bool exact,
+                                           double* acc) {
   constexpr int KG = ChunkGroup<V>::KG;
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
-    float4 v[KG];
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      const unsigned q = tid + (g0 + kk) * NT;
-      v[kk] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
-    }
-    if (!x1bad) {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(fastd(comp(v[kk], e)) * al);
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(static_cast<double>(comp(v[kk], e)) * al);
-    }
-    uint32_t m2 = 0;
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      const unsigned q = tid + (g0 + kk) * NT;
-      if (FULL || q < nq) {
-        if (grow)
-          st_global_v4(grow + q, v[kk], pol);
-        else
-          row[q] = v[kk];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) m2 = nn_max(m2, comp(v[kk], e));
-      }
-    }
-    if (nn_ok(m2)) {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-        if (FULL || tid + (g0 + kk) * NT < nq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += fastd(comp(v[kk], e));
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-        if (FULL || tid + (g0 + kk) * NT < nq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(v[kk], e));
-    }
+    float4 w[KG];
+    load_group<NT, KG, FULL>(row, w, g0, tid, nq);
+    if (exact)
+      group_sweep2<NT, KG, FULL, true>(row, w, g0, tid, nq, al, acc);
+    else
+      group_sweep2<NT, KG, FULL, false>(row, w, g0, tid, nq, al, acc);
   }
 }
 
@@ -251,27 +286,19 @@ __device__ __forceinline__ void row_seed(const float4* row, unsigned tid, unsign
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
     float4 v[KG];
+    load_group<NT, KG, FULL>(row, v, g0, tid, nq);
     uint32_t m = 0;
 #pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      const unsigned q = tid + (g0 + kk) * NT;
-      v[kk] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
+    for (int kk = 0; kk < KG; ++kk)
 #pragma unroll
       for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[kk], e));
-    }
-    if (nn_ok(m)) {
+    const bool ok = nn_ok(m);
 #pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-        if (FULL || tid + (g0 + kk) * NT < nq)
+    for (int kk = 0; kk < KG; ++kk)
+      if (FULL || tid + (g0 + kk) * NT < nq)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += fastd(comp(v[kk], e));
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-        if (FULL || tid + (g0 + kk) * NT < nq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(v[kk], e));
-    }
+        for (int e = 0; e < 4; ++e)
+          acc[4 * (g0 + kk) + e] += ok ? fastd(comp(v[kk], e)) : static_cast<double>(comp(v[kk], e));
   }
 }
 
@@ -289,21 +316,13 @@ struct SweepSmem {
 // thread per row (slice <= 4*NT*V; FULL: equality), BM max rows per batch, NBUF
 // ring slots. LA: batches between sweep 1 and sweep 2 of a batch beyond the
 // next one (the factor warps' latency budget). XCHG: G > 1, row sums are
-// exchanged across the group. SEED: the read-only init_col_sums sweep. STG:
-// sweep 2 stores straight to HBM from registers, so a slot is refilled as soon
-// as sweep 2 has read it (one slot more of lag for the same ring).
-template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED, bool STG = false>
+// exchanged across the group. SEED: the read-only init_col_sums sweep.
+template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED>
 __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const SweepArgs a) {
   constexpr int NW = NT / 32;
   static_assert(NF >= 1 && NF <= kErrSlots, "factor warps");
-  static_assert(LA >= 1 && LA <= 3 && (!XCHG || LA >= 2), "lag");
-  static_assert(NBUF >= LA + (STG ? 3 : 4), "ring too small");
-#ifdef UOT_EARLY_DONE1
-  constexpr bool EARLY_DONE1 = true;
-#else
-  constexpr bool EARLY_DONE1 = false;
-#endif
-  static_assert(!EARLY_DONE1 || LA <= kQ - 2, "alpha/red rings too short for an early done1");
+  static_assert(LA >= 1 && LA <= 2 && (!XCHG || LA == 2), "lag (the alpha / red rings hold kQ batches)");
+  static_assert(NBUF >= LA + 4, "ring too small");
   static_assert(!XCHG || BM == 1, "the exchange path moves one row per batch");
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -398,27 +417,21 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       TR_BEGIN();
       mbar_wait(&done2[b % NBUF], (b / NBUF) & 1u);  // slot b consumed (sweep 2 / seed done)
       TR_END(4);
-      if (SEED || STG) {
+      if (SEED) {
         if (b + NBUF < nb) issue_load(b + NBUF);
         continue;
       }
-      TR_BEGIN();
       issue_store(b);
-      TR_END(5);
       // refill the slot of the previous batch: its store has had a whole batch to drain
       if (b >= 1 && b - 1 + NBUF < nb) {
-        TR_BEGIN();
         bulk_wait_read<1>();
-        TR_END(6);
-        TR_BEGIN();
         issue_load(b - 1 + NBUF);
-        TR_END(7);
       }
     }
-    if (!SEED && !STG) bulk_wait<0>();  // every store landed before the CTA retires
+    if (!SEED) bulk_wait<0>();  // every store landed before the CTA retires
 #ifdef UOT_TRACE
-    tr_acc[8] = clock64() - tr_p0;
-    TR_FLUSH(4, 9);
+    atomicAdd(&uot_trace[8], clock64() - tr_p0);
+    TR_FLUSH(4, 5);
 #endif
     return;
   }
@@ -444,54 +457,33 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       TR_BEGIN();
       mbar_wait(&done1[q], (s / kQ) & 1u);
       TR_END(0);
-#ifdef UOT_NO_FACTOR
-      if (lane < static_cast<int>(nr)) alpha_s[q * BM + lane] = 1.0;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&alpha_rdy[q]);
-      continue;
-#endif
-      TR_BEGIN();
       double t = 0.0;  // this CTA's partial of row `lane` of the batch, warp order
       if (lane < static_cast<int>(nr)) {
         t = red[(q * NW) * BM + lane];
 #pragma unroll
         for (int w = 1; w < NW; ++w) t += red[(q * NW + w) * BM + lane];
       }
-#ifdef UOT_NO_XCHG
-      if (false) {
-#else
       if (XCHG) {
-#endif
         // Publish {partial, tag} for the group, then gather all G partials of
-        // the row and sum them in ascending g (identical bits on every CTA).
-#ifdef UOT_XREC_GROUPED
-        // the G records of one row are adjacent: one 16*G-byte poll per round trip
-        ulonglong2* const xrow = &a.xrec[(static_cast<size_t>(group) * kRing + (s % kRing)) * G];
-        ulonglong2* const xmine = xrow + g;
-        const ulonglong2* const xpeer = xrow + lane;
-#else
-        ulonglong2* const xmine = &a.xrec[static_cast<size_t>(cta) * kRing + (s % kRing)];
-        const ulonglong2* const xpeer = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (s % kRing)];
-#endif
-        if (lane == 0)
-          st_relaxed_b128(xmine,
-                          static_cast<unsigned long long>(__double_as_longlong(t)), tag_hi | (s + 1));
-        TR_END(1);
+        // the row (one lane per CTA, spinning on L2: any back-off costs more
+        // than the polls) and sum them in ascending g: identical bits on every
+        // CTA of the group.
         TR_BEGIN();
+        if (lane == 0)
+          st_relaxed_b128(&a.xrec[static_cast<size_t>(cta) * kRing + (s % kRing)],
+                          static_cast<unsigned long long>(__double_as_longlong(t)), tag_hi | (s + 1));
         double v = 0.0;
         if (lane < static_cast<int>(G)) {
-          const ulonglong2* rec = xpeer;
+          const ulonglong2* rec = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (s % kRing)];
           const unsigned long long want = tag_hi | (s + 1);
           unsigned long long lo, hi;
           ld_relaxed_b128(rec, lo, hi);
           if (hi != want) {
             const unsigned long long t0 = globaltimer_ns();
+            unsigned n = 0;
             do {
-#ifdef UOT_POLL_SLEEP
-              __nanosleep(32);
-#endif
               ld_relaxed_b128(rec, lo, hi);
-              if (hi != want && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
+              if (hi != want && (++n & 255u) == 0 && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
                 atomicOr(&ctl->status, kStatusExchangeTimeout);
                 break;
               }
@@ -503,16 +495,11 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         for (unsigned k = 0; k < G; ++k) tot += __shfl_sync(0xffffffffu, v, k);
         t = tot;
         TR_END(2);
-        TR_BEGIN();
       }
+      TR_BEGIN();
       if (lane < static_cast<int>(nr)) {
         double al;
-#ifdef UOT_NO_POW
-        al = t > 0 ? 1.0 : rv;
-        if (false) {
-#else
         if (!rescale_factor_dev(rv, t, a.fi, &al)) {
-#endif
           atomicOr(&ctl->alpha_bad, 1);
           al = 1.0;
         }
@@ -533,17 +520,19 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         for (int k = NF; k < kErrSlots; ++k) a.cta_err[kErrSlots * cta + k] = 0.0;
     }
 #ifdef UOT_TRACE
-    tr_acc[9] = clock64() - tr_f0;
-    if (lane == 0 && f == 0) { TR_FLUSH(0, 4); TR_FLUSH(9, 10); }
+    if (lane == 0 && f == 0) {
+      TR_FLUSH(0, 4);
+      atomicAdd(&uot_trace[9], clock64() - tr_f0);
+    }
 #endif
     return;
   }
 
   // ========================================================= compute warps ==
-  const uint64_t spol = a.evict_first ? policy_evict_first() : policy_evict_normal();
   double beta[4 * V], acc[4 * V];
 #pragma unroll
   for (int i = 0; i < 4 * V; ++i) acc[i] = 0.0;
+  ScreenBounds sb{0xffffffffu, 0u};
   if (!SEED) {
     const double* bsrc = a.beta2 + ((ctl->iter + 1) & 1ull) * a.pitch + static_cast<size_t>(g) * a.slice;
 #pragma unroll
@@ -552,107 +541,85 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
 #pragma unroll
       for (int e = 0; e < 4; ++e) beta[4 * k + e] = (FULL || q < nq) ? bsrc[4 * q + e] : 1.0;
     }
+    sb = screen_bounds(beta, 4 * V);
   }
 
-  uint64_t x1bad = 0;  // bit (b % 8) * 8 + r: row r of batch b stored a non-normal x1
 #ifdef UOT_TRACE
   const unsigned long long tr_c0 = clock64();
 #endif
-  const unsigned nsteps = SEED ? nb : nb + LA + 1;
-  double part[BM];
-  // Row partials of batch s: warp xor-tree -> smem -> done1 (the factor warps).
-  auto reduce_rows = [&](unsigned s) {
-    if (SEED || s >= nb) return;
-    TR_BEGIN();
-    const unsigned nr = rows_in(s);
-    const unsigned qq = s % kQ;
-#pragma unroll
-    for (int r = 0; r < BM; ++r) {
-      if (r < static_cast<int>(nr)) {
-        const double t = warp_sum(part[r]);
-        if (lane == 0) red[(qq * NW + warp) * BM + r] = t;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&done1[qq]);
-    TR_END(18);
-  };
-  for (unsigned s = 0; s < nsteps; ++s) {
-    // sweep 1 on batch s (or the seed accumulation); its row partials are
-    // reduced before (EARLY_DONE1: the factor chain starts sooner) or after
-    // sweep 2 (the shuffle latency overlaps that work).
-    if (s < nb) {
-      TR_BEGIN();
+  if (SEED) {
+    for (unsigned s = 0; s < nb; ++s) {
       mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
-      TR_END(16);
-      float* buf = slot_ptr(s);
+      const float* buf = slot_ptr(s);
       const unsigned nr = rows_in(s);
-      TR_BEGIN();
-      if (SEED) {
+#pragma unroll
+      for (int r = 0; r < BM; ++r)
+        if (r < static_cast<int>(nr))
+          row_seed<NT, V, FULL>(reinterpret_cast<const float4*>(buf + r * a.slice), tid, nq, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done2[s % NBUF]);
+    }
+  } else {
+    uint64_t x1bad = 0;  // bit (b % 8) * 8 + r: row r of batch b took the exact path in sweep 1
+    for (unsigned s = 0; s < nb + LA + 1; ++s) {
+      const bool s1 = s < nb;                                                    // sweep 1 of batch s
+      const bool s2 = s >= static_cast<unsigned>(LA + 1) && s - (LA + 1) < nb;  // sweep 2 of batch b
+      const unsigned b = s - (LA + 1);
+      double part[BM];
+      if (s1) {
+        TR_BEGIN();
+        mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
+        TR_END(16);
+        float* buf = slot_ptr(s);
+        const unsigned nr = rows_in(s);
+        const unsigned sh = (s % 8) * 8;
+        x1bad &= ~(0xffull << sh);
+#pragma unroll
+        for (int r = 0; r < BM; ++r) {
+          part[r] = 0.0;
+          if (r < static_cast<int>(nr)) {
+            bool bad = false;
+            part[r] = row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, sb, bad);
+            if (bad) x1bad |= 1ull << (sh + r);
+          }
+        }
+      }
+      if (s2) {  // sweep 2 of batch s-1-LA once its factors are published
+        TR_BEGIN();
+        mbar_wait(&alpha_rdy[b % kQ], (b / kQ) & 1u);
+        TR_END(19);
+        float* buf = slot_ptr(b);
+        const unsigned nr = rows_in(b);
+        const unsigned sh = (b % 8) * 8;
 #pragma unroll
         for (int r = 0; r < BM; ++r)
           if (r < static_cast<int>(nr))
-            row_seed<NT, V, FULL>(reinterpret_cast<const float4*>(buf + r * a.slice), tid, nq, acc);
+            row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq,
+                                    alpha_s[(b % kQ) * BM + r], (x1bad >> (sh + r)) & 1ull, acc);
+        fence_proxy_async_smem();  // generic writes -> the producer's bulk store
         __syncwarp();
-        if (lane == 0) mbar_arrive(&done2[s % NBUF]);
-        continue;
+        if (lane == 0) mbar_arrive(&done2[b % NBUF]);
       }
-      const uint32_t shift = (s % 8) * 8;
-      x1bad &= ~(0xffull << shift);
+      if (s1) {  // row partials of batch s (after sweep 2, whose work hides the shuffle latency)
+        const unsigned qq = s % kQ;
+        const unsigned nr = rows_in(s);
 #pragma unroll
-      for (int r = 0; r < BM; ++r) {
-        part[r] = 0.0;
-        if (r < static_cast<int>(nr)) {
-          bool bad = false;
-#ifdef UOT_PIPE_ONLY
-          part[r] = 1.0;
-#else
-          part[r] = row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, bad);
-#endif
-          if (bad) x1bad |= 1ull << (shift + r);
+        for (int r = 0; r < BM; ++r) {
+          if (r < static_cast<int>(nr)) {
+            const double t = warp_sum(part[r]);
+            if (lane == 0) red[(qq * NW + warp) * BM + r] = t;
+          }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done1[qq]);
       }
-      TR_END(17);
     }
-
-    if (EARLY_DONE1) reduce_rows(s);
-
-    // sweep 2 on batch s-1-LA once its factors are published.
-    if (!SEED && s >= static_cast<unsigned>(LA + 1) && s - (LA + 1) < nb) {
-      const unsigned b = s - (LA + 1);
-      const unsigned qb = b % kQ;
-      TR_BEGIN();
-      mbar_wait(&alpha_rdy[qb], (b / kQ) & 1u);
-      TR_END(19);
-      TR_BEGIN();
-      float* buf = slot_ptr(b);
-      const unsigned nr = rows_in(b);
-      const uint32_t shift = (b % 8) * 8;
-#pragma unroll
-      for (int r = 0; r < BM; ++r) {
-#ifndef UOT_PIPE_ONLY
-        if (r < static_cast<int>(nr))
-          row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice),
-                                  STG ? reinterpret_cast<float4*>(gbase + (static_cast<size_t>(b) * B + r) * a.pitch)
-                                      : nullptr,
-                                  spol, tid, nq, alpha_s[qb * BM + r], (x1bad >> (shift + r)) & 1ull, acc);
-#else
-        if (r < static_cast<int>(nr))
-#pragma unroll
-          for (int i = 0; i < 4 * V; ++i) acc[i] += 1.0;
-#endif
-      }
-      if (!STG) fence_proxy_async_smem();  // generic writes -> the producer's bulk store
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&done2[b % NBUF]);
-      TR_END(20);
-    }
-
-    if (!EARLY_DONE1) reduce_rows(s);
   }
 #ifdef UOT_TRACE
-  tr_acc[21] = clock64() - tr_c0;
-  if (tid == 0) { TR_FLUSH(16, 22); }
+  if (tid == 0) {
+    TR_FLUSH(16, 20);
+    atomicAdd(&uot_trace[21], clock64() - tr_c0);
+  }
 #endif
 
   // Column partials of this CTA: one row of the [groups][pitch] table.

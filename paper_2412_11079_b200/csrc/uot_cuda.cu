@@ -19,6 +19,7 @@
 #include "finalize.cuh"
 #include "problem.cuh"
 #include "sweep.cuh"
+#include "sweep_tmem.cuh"
 
 using namespace uotk;
 
@@ -32,15 +33,20 @@ using SweepFn = void (*)(const SweepArgs);
 struct SweepCfg {
   int nt, v, bm, nbuf, nf;
   bool xchg;           // rows span G > 1 CTAs (cross-CTA row-sum exchange)
-  SweepFn iter[2];     // [FULL]
+  SweepFn iter[2];     // [FULL] smem-ring iteration kernel (sweep.cuh)
   SweepFn seed[2];     // [FULL]
+  SweepFn iter_tm[2];  // [FULL] TMEM-lag iteration kernel (sweep_tmem.cuh)
+  int la_tm;
   size_t (*smem_bytes)(unsigned buf_stride);
+  size_t (*smem_bytes_tm)(unsigned buf_stride);
 };
 
-// G == 1: sweep 2 lags sweep 1 by LA=1 extra batch (the factor warps' budget).
-// G > 1: LA=2, the row partials are exchanged across the group.
-// NF factor warps alternate batches: 2 when a batch is one row (a pow and, for
-// G > 1, an L2 round trip per batch), else 1 (the B rows of a batch run on lanes).
+// Sweep 2 lags sweep 1 by LA = 2 extra batches (the factor warps' budget: the
+// pow and, for G > 1, the L2 exchange round trip). NF factor warps alternate
+// batches: 3 for G == 1, 2 when G > 1 (measured: more warps polling L2 cost
+// more issue slots than they buy).
+// TMEM-lag variant (sweep_tmem.cuh, UOT_TMEM=1): measured 2-3% slower than the
+// smem-ring kernel on B200 (profiles/r01_ncu_v3.md), kept as an opt-in.
 #ifndef UOT_LA_G1
 #define UOT_LA_G1 2
 #endif
@@ -50,8 +56,21 @@ struct SweepCfg {
 #ifndef UOT_NF_X
 #define UOT_NF_X 2
 #endif
-#ifndef UOT_STG
-#define UOT_STG 0
+// TMEM-lag kernel: lag (batches in TMEM) and the load / store ring split.
+#ifndef UOT_TM_LA_X
+#define UOT_TM_LA_X 4
+#endif
+#ifndef UOT_TM_LA_G1
+#define UOT_TM_LA_G1 3
+#endif
+#ifndef UOT_TM_NL
+#define UOT_TM_NL 4
+#endif
+#ifndef UOT_TM_NS
+#define UOT_TM_NS 3
+#endif
+#ifndef UOT_TM_S2FIRST
+#define UOT_TM_S2FIRST 1
 #endif
 template <int NT, int V, int BM, int NB, bool XCHG = false>
 SweepCfg make_cfg() {
@@ -67,11 +86,17 @@ SweepCfg make_cfg() {
   c.nbuf = NB;
   c.nf = NF;
   c.xchg = XCHG;
-  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false, UOT_STG>;
-  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false, UOT_STG>;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false>;
   c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true>;
   c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
+  static_assert(UOT_TM_NL + UOT_TM_NS == NB, "TMEM kernel rings use the same shared memory");
+  constexpr int LAT = XCHG ? UOT_TM_LA_X : UOT_TM_LA_G1;
+  c.la_tm = LAT;
+  c.iter_tm[0] = sweep_tmem_kernel<NT, V, BM, UOT_TM_NL, UOT_TM_NS, LAT, XCHG, NF, false, UOT_TM_S2FIRST>;
+  c.iter_tm[1] = sweep_tmem_kernel<NT, V, BM, UOT_TM_NL, UOT_TM_NS, LAT, XCHG, NF, true, UOT_TM_S2FIRST>;
+  c.smem_bytes_tm = &TmemSweepSmem<NT / 32, BM, UOT_TM_NL, UOT_TM_NS>::bytes;
   return c;
 }
 
@@ -172,6 +197,8 @@ struct uot_ctx {
   int evict_first = 0;
   int full = 0;
   int smid_map = 0;
+  size_t smem_tm = 0;    // dynamic smem of the TMEM-lag iteration kernel
+  bool use_tmem = false;  // iterations run sweep_tmem_kernel (opt-in: UOT_TMEM=1)
 
   // device buffers
   float* P = nullptr;
@@ -268,6 +295,11 @@ int plan_layout(uot_ctx* ctx) {
   ctx->grid = ctx->groups * G;
   ctx->buf_stride = round_up(ctx->B * slice * 4u, 128);
   ctx->smem = cfg->smem_bytes(ctx->buf_stride);
+  ctx->smem_tm = cfg->smem_bytes_tm(ctx->buf_stride);
+  int smem_optin = 0;
+  CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  // the TMEM-lag kernel's rings + factor rings must fit next to each other
+  ctx->use_tmem = env_int("UOT_TMEM", 0) != 0 && ctx->smem_tm <= static_cast<size_t>(smem_optin);
   ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * 4 > (64ull << 20) ? 1 : 0;
   ctx->full = slice == static_cast<unsigned>(4 * cfg->nt * cfg->v) ? 1 : 0;
   int rc = probe_smid_map(ctx);
@@ -280,6 +312,9 @@ int plan_layout(uot_ctx* ctx) {
                              "cudaFuncSetAttribute(smem)");
     if (rc) return rc;
   }
+  if (ctx->use_tmem)
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(cfg->iter_tm[ctx->full]),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_tm)));
   return UOT_OK;
 }
 
@@ -376,12 +411,13 @@ FinalizeArgs fin_args(const uot_ctx* ctx) {
 int launch_sweep(uot_ctx* ctx, bool seed) {
   const SweepArgs a = sweep_args(ctx);
   const bool xchg = !seed && ctx->G > 1;
-  SweepFn fn = seed ? ctx->cfg->seed[ctx->full] : ctx->cfg->iter[ctx->full];
+  const bool tm = !seed && ctx->use_tmem;
+  SweepFn fn = seed ? ctx->cfg->seed[ctx->full] : (tm ? ctx->cfg->iter_tm[ctx->full] : ctx->cfg->iter[ctx->full]);
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctx->grid);
   // compute warps + producer warp + factor warp(s)
   lc.blockDim = dim3(ctx->cfg->nt + 32 * (1 + (seed ? 1 : ctx->cfg->nf)));
-  lc.dynamicSmemBytes = ctx->smem;
+  lc.dynamicSmemBytes = tm ? ctx->smem_tm : ctx->smem;
   lc.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // CTAs of a group spin on each other
@@ -670,7 +706,8 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->rows_per_step = ctx->B;
   o->threads = ctx->cfg->nt + 32 * (1 + ctx->cfg->nf);
   o->chunks = ctx->cfg->v;
-  o->smem_bytes = static_cast<uint32_t>(ctx->smem);
+  o->smem_bytes = static_cast<uint32_t>(ctx->use_tmem ? ctx->smem_tm : ctx->smem);
+  o->tmem = ctx->use_tmem ? 1 : 0;
   o->nbuf = ctx->cfg->nbuf;
   o->sms = ctx->sms;
   o->rank = ctx->rank;

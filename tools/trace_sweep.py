@@ -10,10 +10,9 @@ sys.path.insert(0, ".")
 os.environ.setdefault("UOT_LIB_PATH", os.path.abspath("paper_2412_11079_b200/libuot_cuda_trace.so"))
 from paper_2412_11079_b200 import uot  # noqa: E402
 
-NAMES = {0: "ctl wait done1", 1: "ctl alpha (G=1)/publish", 2: "ctl poll", 3: "ctl pow+arrive (xchg)",
-         4: "ctl wait done2", 5: "ctl issue store", 6: "ctl wait_read", 7: "ctl issue load", 8: "ctl TOTAL",
-         16: "w0 wait full", 17: "w0 sweep1", 18: "w0 reduce+arrive", 19: "w0 wait alpha", 20: "w0 sweep2",
-         21: "w0 TOTAL"}
+NAMES = {0: "factor0 wait done1", 2: "factor0 exchange poll", 3: "factor0 pow+arrive", 9: "factor0 TOTAL",
+         4: "producer wait done2", 8: "producer TOTAL",
+         16: "warp0 wait full", 19: "warp0 wait alpha", 21: "warp0 TOTAL"}
 L = uot.lib()
 L.uot_trace_read.argtypes = [C.c_void_p, C.c_int]
 buf = (C.c_ulonglong * 32)()
@@ -31,8 +30,10 @@ for spec in sys.argv[1:]:
         lay = s.layout
         grid = lay["groups"] * lay["G"]
         nb = (m / lay["groups"]) / lay["rows_per_step"]
+        nbf = {0: 2, 2: 2, 3: 2, 9: 1}  # factor warp 0 handles every NF-th batch (NF = 2 for these shapes)
         print(f"== {m}x{n} x{k}: sweep {sw / cnt:.3f} ms ({2 * m * n * 4 / (sw / cnt * 1e-3) / 1e9:.0f} GB/s) "
               f"G={lay['G']} groups={lay['groups']} B={lay['rows_per_step']} nbuf={lay['nbuf']} batches/CTA={nb:.0f}")
         for i, name in NAMES.items():
             v = buf[i] / (grid * k)
-            print(f"   {name:28s} {v / 1e3:10.1f} kcyc/CTA/iter  {v / nb:8.0f} cyc/batch")
+            per = v / nb * (nbf.get(i, 1) if i != 9 else 1)
+            print(f"   {name:28s} {v / 1e3:10.1f} kcyc/CTA/iter  {v / nb:8.0f} cyc/batch (all batches)")
