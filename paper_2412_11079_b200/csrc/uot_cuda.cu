@@ -20,6 +20,7 @@
 #include "problem.cuh"
 #include "sweep.cuh"
 #include "sweep_tmem.cuh"
+#include "resident.cuh"
 
 using namespace uotk;
 
@@ -98,6 +99,29 @@ SweepCfg make_cfg() {
   c.iter_tm[1] = sweep_tmem_kernel<NT, V, BM, UOT_TM_NL, UOT_TM_NS, LAT, XCHG, NF, true, UOT_TM_S2FIRST>;
   c.smem_bytes_tm = &TmemSweepSmem<NT / 32, BM, UOT_TM_NL, UOT_TM_NS>::bytes;
   return c;
+}
+
+// Resident (whole solve in one launch, matrix in shared memory) variants.
+using ResidentFn = void (*)(const ResidentArgs);
+struct ResidentCfg {
+  int nt, v;
+  ResidentFn fn[2];  // [FULL]
+  size_t (*smem_bytes)(unsigned rows_cta, unsigned pitch);
+};
+template <int NT, int V>
+ResidentCfg make_rcfg() {
+  ResidentCfg c{};
+  c.nt = NT;
+  c.v = V;
+  c.fn[0] = resident_kernel<NT, V, false>;
+  c.fn[1] = resident_kernel<NT, V, true>;
+  c.smem_bytes = &ResidentSmem<NT, V>::bytes;
+  return c;
+}
+const std::vector<ResidentCfg>& rcfg_table() {
+  static const std::vector<ResidentCfg> t = {make_rcfg<128, 1>(), make_rcfg<256, 1>(), make_rcfg<512, 1>(),
+                                             make_rcfg<512, 2>(), make_rcfg<512, 4>()};
+  return t;
 }
 
 const std::vector<SweepCfg>& cfg_table() {
@@ -198,6 +222,11 @@ struct uot_ctx {
   int full = 0;
   int smid_map = 0;
   size_t smem_tm = 0;    // dynamic smem of the TMEM-lag iteration kernel
+  // resident mode: the whole uot_iterate call is one persistent launch
+  const ResidentCfg* rcfg = nullptr;
+  unsigned rgrid = 0;
+  size_t rsmem = 0;
+  int rfull = 0;
   bool use_tmem = false;  // iterations run sweep_tmem_kernel (opt-in: UOT_TMEM=1)
 
   // device buffers
@@ -207,6 +236,7 @@ struct uot_ctx {
   ulonglong2* xrec = nullptr;
   Control* ctl = nullptr;
   int* dflag = nullptr;
+  unsigned* bar_flags = nullptr;  // resident kernel's grid barrier (one epoch per CTA)
   Control* h_ctl = nullptr;  // pinned mirror
 
   double fi = 0.0;
@@ -315,6 +345,27 @@ int plan_layout(uot_ctx* ctx) {
   if (ctx->use_tmem)
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(cfg->iter_tm[ctx->full]),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_tm)));
+  // Resident mode (resident.cuh): one rank, rows fit one CTA (G == 1), a CTA's
+  // row block fits shared memory and at most 32 rows per CTA. UOT_RESIDENT=0: off.
+  ctx->rcfg = nullptr;
+  if (ctx->nranks == 1 && G == 1 && env_int("UOT_RESIDENT", 1)) {
+    const unsigned rgrid = static_cast<unsigned>(std::min<uint64_t>(ctx->rows, ctx->sms));
+    const uint64_t rows_cta = (ctx->rows + rgrid - 1) / rgrid;
+    const unsigned nq = ctx->pitch / 4;
+    for (const auto& rc : rcfg_table()) {
+      if (static_cast<unsigned>(rc.nt * rc.v) < nq) continue;
+      const size_t sm = rc.smem_bytes(static_cast<unsigned>(rows_cta), ctx->pitch);
+      if (rows_cta <= 32 && sm <= static_cast<size_t>(smem_optin)) {
+        ctx->rcfg = &rc;
+        ctx->rgrid = rgrid;
+        ctx->rsmem = sm;
+        ctx->rfull = nq == static_cast<unsigned>(rc.nt * rc.v) ? 1 : 0;
+        CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(rc.fn[ctx->rfull]),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      }
+      break;
+    }
+  }
   return UOT_OK;
 }
 
@@ -340,6 +391,8 @@ int alloc_all(uot_ctx* ctx) {
   if ((rc = dalloc(ctx, &ctx->xrec, xn))) return rc;
   if ((rc = dalloc(ctx, &ctx->ctl, 1))) return rc;
   if ((rc = dalloc(ctx, &ctx->dflag, 1))) return rc;
+  if ((rc = dalloc(ctx, &ctx->bar_flags, std::max<size_t>(ctx->grid, ctx->sms)))) return rc;
+  CK(cudaMemsetAsync(ctx->bar_flags, 0, std::max<size_t>(ctx->grid, ctx->sms) * sizeof(unsigned), ctx->stream));
   if ((rc = ctx->cuda(cudaMallocHost(&ctx->h_ctl, sizeof(Control)), "cudaMallocHost"))) return rc;
   CK(cudaMemsetAsync(ctx->xrec, 0, xn * sizeof(ulonglong2), ctx->stream));
   CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Control), ctx->stream));
@@ -426,6 +479,38 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
   lc.numAttrs = xchg ? 1 : 0;
   ctx->launches++;
   return ctx->cuda(cudaLaunchKernelEx(&lc, fn, a), "sweep launch");
+}
+
+// The whole iterate(k) call as one cooperative launch (resident.cuh).
+int launch_resident(uot_ctx* ctx, uint64_t k) {
+  ResidentArgs r;
+  r.P = ctx->P;
+  r.beta2 = ctx->beta2;
+  r.rpd = ctx->rpd;
+  r.cpd = ctx->cpd;
+  r.alpha = ctx->alpha;
+  r.partials = ctx->partials;
+  r.col_sums = ctx->col_sums;
+  r.bar_flags = ctx->bar_flags;
+  r.ctl = ctx->ctl;
+  r.rows = ctx->rows;
+  r.cols = static_cast<unsigned>(ctx->cols);
+  r.pitch = ctx->pitch;
+  r.grid = ctx->rgrid;
+  r.k = static_cast<unsigned>(std::min<uint64_t>(k, 0xffffffffu));
+  r.fi = ctx->fi;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(ctx->rgrid);
+  lc.blockDim = dim3(ctx->rcfg->nt);
+  lc.dynamicSmemBytes = ctx->rsmem;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers need every CTA resident
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  ctx->launches++;
+  return ctx->cuda(cudaLaunchKernelEx(&lc, ctx->rcfg->fn[ctx->rfull], r), "resident launch");
 }
 
 template <int MODE>
@@ -683,7 +768,7 @@ void uot_destroy(uot_ctx* ctx) {
   if (ctx->d_peers) cudaFree(ctx->d_peers);
   for (auto e : ctx->ev) cudaEventDestroy(e);
   void* bufs[] = {ctx->P,     ctx->rpd,   ctx->cpd,      ctx->alpha,   ctx->beta2, ctx->col_sums, ctx->xsum,
-                  ctx->partials, ctx->cta_err, ctx->xrec, ctx->ctl, ctx->dflag};
+                  ctx->partials, ctx->cta_err, ctx->xrec, ctx->ctl, ctx->dflag, ctx->bar_flags};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -708,6 +793,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->chunks = ctx->cfg->v;
   o->smem_bytes = static_cast<uint32_t>(ctx->use_tmem ? ctx->smem_tm : ctx->smem);
   o->tmem = ctx->use_tmem ? 1 : 0;
+  o->resident = ctx->rcfg ? 1 : 0;
   o->nbuf = ctx->cfg->nbuf;
   o->sms = ctx->sms;
   o->rank = ctx->rank;
@@ -848,12 +934,19 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
   ctx->launches++;
   CK(cudaGetLastError());
   int rc;
-  for (uint64_t i = 0; i < k; ++i) {
-    if (ctx->timing) record(ctx, 3 * i);
-    if ((rc = launch_sweep(ctx, false))) return rc;
-    if (ctx->timing) record(ctx, 3 * i + 1);
-    if ((rc = launch_finalize<kFinIter>(ctx))) return rc;
-    if (ctx->timing) record(ctx, 3 * i + 2);
+  const bool resident = ctx->rcfg != nullptr;
+  if (resident) {  // k iterations, one launch: sweep + reduction + stop test inside
+    if (ctx->timing) record(ctx, 0);
+    if ((rc = launch_resident(ctx, k))) return rc;
+    if (ctx->timing) record(ctx, 1);
+  } else {
+    for (uint64_t i = 0; i < k; ++i) {
+      if (ctx->timing) record(ctx, 3 * i);
+      if ((rc = launch_sweep(ctx, false))) return rc;
+      if (ctx->timing) record(ctx, 3 * i + 1);
+      if ((rc = launch_finalize<kFinIter>(ctx))) return rc;
+      if (ctx->timing) record(ctx, 3 * i + 2);
+    }
   }
   if (device_ms) CK(cudaEventRecord(t1, ctx->stream));
   if ((rc = sync_ctl(ctx))) return rc;
@@ -866,14 +959,19 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
   }
   if (ctx->timing) {
     ctx->sweep_ms = ctx->fin_ms = 0.0;
-    for (uint64_t i = 0; i < k; ++i) {
+    if (resident) {  // one launch: reported as sweep time, no separate finalize
+      float a = 0.f;
+      cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+      ctx->sweep_ms = a;
+    }
+    for (uint64_t i = 0; i < (resident ? 0 : k); ++i) {
       float a = 0.f, b = 0.f;
       cudaEventElapsedTime(&a, ctx->ev[3 * i], ctx->ev[3 * i + 1]);
       cudaEventElapsedTime(&b, ctx->ev[3 * i + 1], ctx->ev[3 * i + 2]);
       ctx->sweep_ms += a;
       ctx->fin_ms += b;
     }
-    ctx->sweeps_timed = k;
+    ctx->sweeps_timed = resident ? std::max<uint64_t>(1, ctx->h_ctl->iter - before) : k;
   }
   if (iterations) *iterations = ctx->h_ctl->iter - before;
   if (final_error) *final_error = ctx->h_ctl->last_error;

@@ -34,7 +34,11 @@ struct Control {
   int beta_bad_next;          // being produced by the running finalize
   int alpha_bad;              // a row factor of the running sweep degenerated
   unsigned int fin_count;     // last-block election in finalize
+  unsigned int bar_count;     // grid barrier of the resident kernel (arrivals)
+  unsigned int bar_gen;       // grid barrier generation (never reset)
   unsigned int pad_;
+  double rerr_beta[3];        // resident kernel: max|beta(t)-1| at slot t%3
+  double rerr_alpha[3];       // resident kernel: max|alpha(t)-1| at slot t%3
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -12,7 +12,10 @@ from paper_2412_11079_b200 import uot  # noqa: E402
 
 NAMES = {0: "factor0 wait done1", 2: "factor0 exchange poll", 3: "factor0 pow+arrive", 9: "factor0 TOTAL",
          4: "producer wait done2", 8: "producer TOTAL",
-         16: "warp0 wait full", 19: "warp0 wait alpha", 21: "warp0 TOTAL"}
+         16: "warp0 wait full", 19: "warp0 wait alpha", 21: "warp0 TOTAL",
+         24: "resident: beta load", 25: "resident: sweep 1", 26: "resident: factors (pow)",
+         27: "resident: sweep 2 + partials", 28: "resident: barrier 1", 29: "resident: column reduction",
+         30: "resident: barrier 2"}
 L = uot.lib()
 L.uot_trace_read.argtypes = [C.c_void_p, C.c_int]
 buf = (C.c_ulonglong * 32)()
@@ -34,6 +37,10 @@ for spec in sys.argv[1:]:
         print(f"== {m}x{n} x{k}: sweep {sw / cnt:.3f} ms ({2 * m * n * 4 / (sw / cnt * 1e-3) / 1e9:.0f} GB/s) "
               f"G={lay['G']} groups={lay['groups']} B={lay['rows_per_step']} nbuf={lay['nbuf']} batches/CTA={nb:.0f}")
         for i, name in NAMES.items():
+            if i >= 24:  # one CTA's per-iteration phase times
+                if lay.get("resident"):
+                    print(f"   {name:28s} {buf[i] / k / 1965:8.2f} us/iter")
+                continue
             v = buf[i] / (grid * k)
             per = v / nb * (nbf.get(i, 1) if i != 9 else 1)
             print(f"   {name:28s} {v / 1e3:10.1f} kcyc/CTA/iter  {v / nb:8.0f} cyc/batch (all batches)")
