@@ -100,6 +100,18 @@ UOT_API int uot_peer_connect(uot_ctx* ctx, const uint8_t* handles);
 /* 0 single GPU, 1 NCCL allreduce, 2 fused peer-memory exchange. */
 UOT_API int uot_exchange_mode(const uot_ctx* ctx);
 
+/* Iteration schedule of uot_iterate (single GPU). FUSED is the product path
+ * (fused_iterate_parallel, fused.hpp:197-250: one read + one write of P per
+ * iteration). TWO_PASS is the paper's GPU data flow emulated by tiled_iterate
+ * (tiled.hpp:210-229: part4 -> row factors -> part2, 2 reads + 2 writes) and
+ * BASELINE the reference's four-sweep baseline_iterate (baseline.hpp:100-110:
+ * 4 reads + 2 writes) — ablations that measure the traffic model of
+ * metrics.cpp:60-77 on HBM. All three compute the same iteration. */
+#define UOT_VARIANT_FUSED 0
+#define UOT_VARIANT_TWO_PASS 1
+#define UOT_VARIANT_BASELINE 2
+UOT_API int uot_set_variant(uot_ctx* ctx, int variant);
+
 UOT_API void uot_destroy(uot_ctx* ctx);
 UOT_API const char* uot_last_error(const uot_ctx* ctx);
 UOT_API int uot_get_layout(const uot_ctx* ctx, uot_layout* out);

@@ -21,6 +21,7 @@
 #include "sweep.cuh"
 #include "sweep_tmem.cuh"
 #include "resident.cuh"
+#include "ablation.cuh"
 
 using namespace uotk;
 
@@ -237,6 +238,10 @@ struct uot_ctx {
   Control* ctl = nullptr;
   int* dflag = nullptr;
   unsigned* bar_flags = nullptr;  // resident kernel's grid barrier (one epoch per CTA)
+  // iteration schedule (uot_set_variant): fused sweep, or the two ablations
+  int variant = UOT_VARIANT_FUSED;
+  double *abl_partials = nullptr, *abl_row_err = nullptr;
+  unsigned abl_gx = 0, abl_gy = 0, abl_rowctas = 0;
   Control* h_ctl = nullptr;  // pinned mirror
 
   double fi = 0.0;
@@ -479,6 +484,57 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
   lc.numAttrs = xchg ? 1 : 0;
   ctx->launches++;
   return ctx->cuda(cudaLaunchKernelEx(&lc, fn, a), "sweep launch");
+}
+
+// ------------------------------------------------------------ ablations --
+AblArgs abl_args(const uot_ctx* ctx) {
+  AblArgs a;
+  a.P = ctx->P;
+  a.beta2 = ctx->beta2;
+  a.rpd = ctx->rpd;
+  a.alpha = ctx->alpha;
+  a.partials = ctx->abl_partials;
+  a.row_err = ctx->abl_row_err;
+  a.ctl = ctx->ctl;
+  a.rows = ctx->rows;
+  a.cols = static_cast<unsigned>(ctx->cols);
+  a.pitch = ctx->pitch;
+  a.gy = ctx->abl_gy;
+  a.fi = ctx->fi;
+  return a;
+}
+
+FinalizeArgs abl_fin_args(const uot_ctx* ctx) {
+  FinalizeArgs f = fin_args(ctx);
+  f.partials = ctx->abl_partials;
+  f.groups = ctx->abl_gy;
+  f.cta_err = ctx->abl_row_err;
+  f.grid = (ctx->abl_rowctas + kErrSlots - 1) / kErrSlots;  // row_err is zero padded
+  return f;
+}
+
+// One iteration of the two-pass (tiled.hpp:210-229) or four-sweep baseline
+// (baseline.hpp:100-110) schedule; see ablation.cuh.
+int launch_ablation_iteration(uot_ctx* ctx) {
+  const AblArgs a = abl_args(ctx);
+  const dim3 cg(ctx->abl_gx, ctx->abl_gy);
+  const unsigned rg = ctx->abl_rowctas, rt = 32 * kAblRowWarps;
+  const unsigned fb = finalize_blocks(ctx->pitch);
+  if (ctx->variant == UOT_VARIANT_TWO_PASS) {
+    abl_row_kernel<true, true, false><<<rg, rt, 0, ctx->stream>>>(a);          // part4 -> alpha
+    abl_col_kernel<true, false, true><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // part2 -> column partials
+    finalize_kernel<kFinIter, true, true><<<fb, kFinThreads, 0, ctx->stream>>>(abl_fin_args(ctx));
+    ctx->launches += 3;
+  } else {
+    abl_col_kernel<false, false, true><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // column sums
+    finalize_kernel<kFinSeed, true, true><<<fb, kFinThreads, 0, ctx->stream>>>(abl_fin_args(ctx));  // beta(t)
+    abl_col_kernel<false, true, false><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // column scaling
+    abl_row_kernel<false, true, false><<<rg, rt, 0, ctx->stream>>>(a);             // row sums -> alpha
+    abl_row_kernel<false, false, true><<<rg, rt, 0, ctx->stream>>>(a);             // row scaling
+    abl_baseline_tail_kernel<<<1, 256, 0, ctx->stream>>>(a, rg);
+    ctx->launches += 6;
+  }
+  return ctx->cuda(cudaGetLastError(), "ablation launch");
 }
 
 // The whole iterate(k) call as one cooperative launch (resident.cuh).
@@ -755,6 +811,28 @@ int uot_peer_connect(uot_ctx* ctx, const uint8_t* handles) {
 
 int uot_exchange_mode(const uot_ctx* ctx) { return ctx ? ctx->xmode : -1; }
 
+int uot_set_variant(uot_ctx* ctx, int variant) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  if (variant != UOT_VARIANT_FUSED && variant != UOT_VARIANT_TWO_PASS && variant != UOT_VARIANT_BASELINE)
+    return ctx->fail(UOT_INVALID_PARAMETER, "unknown iteration variant %d", variant);
+  if (variant != UOT_VARIANT_FUSED && ctx->nranks > 1)
+    return ctx->fail(UOT_INVALID_PARAMETER, "the ablation schedules are single-GPU only");
+  CK(cudaSetDevice(ctx->device));
+  if (variant != UOT_VARIANT_FUSED && !ctx->abl_partials) {
+    ctx->abl_gx = (ctx->pitch / 4 + kAblColThreads * kAblColV - 1) / (kAblColThreads * kAblColV);
+    ctx->abl_gy = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>(ctx->rows, (4u * ctx->sms + ctx->abl_gx - 1) / ctx->abl_gx)));
+    ctx->abl_rowctas = static_cast<unsigned>((ctx->rows + kAblRowWarps - 1) / kAblRowWarps);
+    const size_t nerr = (ctx->abl_rowctas + kErrSlots - 1) / kErrSlots * kErrSlots;
+    int rc;
+    if ((rc = dalloc(ctx, &ctx->abl_partials, static_cast<size_t>(ctx->abl_gy) * ctx->pitch))) return rc;
+    if ((rc = dalloc(ctx, &ctx->abl_row_err, nerr))) return rc;
+    CK(cudaMemsetAsync(ctx->abl_row_err, 0, nerr * sizeof(double), ctx->stream));
+  }
+  ctx->variant = variant;
+  return UOT_OK;
+}
+
 void uot_destroy(uot_ctx* ctx) {
   if (!ctx) return;
   if (ctx->stream) {
@@ -768,7 +846,8 @@ void uot_destroy(uot_ctx* ctx) {
   if (ctx->d_peers) cudaFree(ctx->d_peers);
   for (auto e : ctx->ev) cudaEventDestroy(e);
   void* bufs[] = {ctx->P,     ctx->rpd,   ctx->cpd,      ctx->alpha,   ctx->beta2, ctx->col_sums, ctx->xsum,
-                  ctx->partials, ctx->cta_err, ctx->xrec, ctx->ctl, ctx->dflag, ctx->bar_flags};
+                  ctx->partials, ctx->cta_err, ctx->xrec, ctx->ctl, ctx->dflag, ctx->bar_flags,
+                  ctx->abl_partials, ctx->abl_row_err};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -934,8 +1013,15 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
   ctx->launches++;
   CK(cudaGetLastError());
   int rc;
-  const bool resident = ctx->rcfg != nullptr;
-  if (resident) {  // k iterations, one launch: sweep + reduction + stop test inside
+  const bool resident = ctx->rcfg != nullptr && ctx->variant == UOT_VARIANT_FUSED;
+  if (ctx->variant != UOT_VARIANT_FUSED) {
+    for (uint64_t i = 0; i < k; ++i) {
+      if (ctx->timing) record(ctx, 3 * i);
+      if ((rc = launch_ablation_iteration(ctx))) return rc;
+      if (ctx->timing) record(ctx, 3 * i + 1);
+      if (ctx->timing) record(ctx, 3 * i + 2);
+    }
+  } else if (resident) {  // k iterations, one launch: sweep + reduction + stop test inside
     if (ctx->timing) record(ctx, 0);
     if ((rc = launch_resident(ctx, k))) return rc;
     if (ctx->timing) record(ctx, 1);

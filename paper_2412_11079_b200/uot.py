@@ -115,6 +115,7 @@ def lib():
     L.uot_peer_handle.argtypes = [_P, _P]
     L.uot_peer_connect.argtypes = [_P, _P]
     L.uot_exchange_mode.argtypes = [_P]
+    L.uot_set_variant.argtypes = [_P, _i]
     L.uot_destroy.argtypes = [_P]
     L.uot_destroy.restype = None
     L.uot_last_error.argtypes = [_P]
@@ -439,6 +440,15 @@ class Session:
         calls, dbl = _u64(), _u64()
         self._check(lib().uot_get_comm_stats(self._h, C.byref(calls), C.byref(dbl)))
         return int(calls.value), int(dbl.value)
+
+    VARIANTS = {"fused": 0, "two_pass": 1, "baseline": 2}
+
+    def set_variant(self, name: str):
+        """Iteration schedule: "fused" (the product), or the ablations "two_pass"
+        (tiled.hpp:210-229) and "baseline" (baseline.hpp:100-110)."""
+        if name not in self.VARIANTS:
+            _raise(1, f"unknown iteration variant {name!r}")
+        self._check(lib().uot_set_variant(self._h, self.VARIANTS[name]))
 
     def set_timing(self, on: bool = True):
         self._check(lib().uot_set_timing(self._h, 1 if on else 0))
