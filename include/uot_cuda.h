@@ -34,6 +34,7 @@ extern "C" {
 #define UOT_CONFIG_ERROR 4      /* uot::ConfigError (launch configuration cannot cover the matrix) */
 #define UOT_CUDA_ERROR 5        /* CUDA runtime failure (no reference analogue) */
 #define UOT_NCCL_ERROR 6        /* NCCL failure (no reference analogue) */
+#define UOT_IO_ERROR 7          /* uot::IoError (problem file container) */
 
 /* Dtype codes: uot::Dtype (include/uot/matrix.hpp:13). Only f32 has a kernel. */
 #define UOT_F32 1
@@ -99,6 +100,22 @@ UOT_API int uot_peer_handle(const uot_ctx* ctx, uint8_t* out64);
 UOT_API int uot_peer_connect(uot_ctx* ctx, const uint8_t* handles);
 /* 0 single GPU, 1 NCCL allreduce, 2 fused peer-memory exchange. */
 UOT_API int uot_exchange_mode(const uot_ctx* ctx);
+
+/* ---- problem files (.uotp, problem_io.cpp:13-141) --------------------- */
+
+/* read_problem's header checks (problem_io.cpp:106-135) without the payload:
+ * extents, dtype (1 f32, 2 f64) and coefficients. UOT_IO_ERROR on a malformed
+ * container; the message is uot_last_io_error(). Host only. */
+UOT_API int uot_problem_file_info(const char* path, uint64_t* m, uint64_t* n, int* dtype, double* er, double* ep);
+UOT_API const char* uot_last_io_error(void);
+/* read_problem + uot_set_problem for this session's row block: the rows of this
+ * rank are streamed from the file to HBM through page-locked staging (the
+ * global matrix is never materialised on the host). f32 files only. */
+UOT_API int uot_load_problem_file(uot_ctx* ctx, const char* path);
+/* write_problem of the session's CURRENT plan with its marginals and er/ep, the
+ * reference's container byte for byte. Multi-rank: every rank writes its rows
+ * and rpd slice, rank 0 the header and cpd (collective on the path). */
+UOT_API int uot_save_problem_file(uot_ctx* ctx, const char* path);
 
 /* Iteration schedule of uot_iterate (single GPU). FUSED is the product path
  * (fused_iterate_parallel, fused.hpp:197-250: one read + one write of P per

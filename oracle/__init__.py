@@ -209,6 +209,10 @@ class RefOracle:
         L.ref_compute_fi.argtypes = [_d, _d, C.POINTER(_d)]
         L.ref_rescale_factor.argtypes = [_d, _d, _d, C.POINTER(_d)]
         L.ref_rank_partition.argtypes = [_sz, _sz, _P]
+        L.ref_write_problem_f32.argtypes = [C.c_char_p, _P, _sz, _sz, _P, _P, _d, _d]
+        L.ref_write_problem_f64.argtypes = [C.c_char_p, _P, _sz, _sz, _P, _P, _d, _d]
+        L.ref_read_problem_f32.argtypes = [C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(_i),
+                                           C.POINTER(_d), C.POINTER(_d), _P, _P, _P]
 
     def _check(self, code):
         if code != 0:
@@ -235,6 +239,27 @@ class RefOracle:
         b = np.zeros(max(ranks, 0) + 1, np.uint64)
         self._check(self.lib.ref_rank_partition(ranks, rows, _ptr(b)))
         return [int(x) for x in b]
+
+    def write_problem(self, path, a, rpd, cpd, er, ep):
+        """uot::write_problem (problem_io.cpp:97-104), f32 or f64 by the dtype of `a`."""
+        a = np.ascontiguousarray(a)
+        fn = self.lib.ref_write_problem_f32 if a.dtype == np.float32 else self.lib.ref_write_problem_f64
+        self._check(fn(os.fsencode(path), _ptr(a), a.shape[0], a.shape[1], _ptr(np.ascontiguousarray(rpd, np.float64)),
+                       _ptr(np.ascontiguousarray(cpd, np.float64)), er, ep))
+
+    def read_problem(self, path):
+        """uot::read_problem (problem_io.cpp:106-141): (dtype, er, ep, a, rpd, cpd); f64 payload not returned."""
+        m, n, dt, er, ep = _sz(), _sz(), _i(), _d(), _d()
+        self._check(self.lib.ref_read_problem_f32(os.fsencode(path), C.byref(m), C.byref(n), C.byref(dt),
+                                                  C.byref(er), C.byref(ep), None, None, None))
+        if dt.value != 1:
+            return "f64", er.value, ep.value, None, None, None
+        a = np.empty((m.value, n.value), np.float32)
+        rpd = np.empty(m.value, np.float64)
+        cpd = np.empty(n.value, np.float64)
+        self._check(self.lib.ref_read_problem_f32(os.fsencode(path), C.byref(m), C.byref(n), C.byref(dt),
+                                                  C.byref(er), C.byref(ep), _ptr(a), _ptr(rpd), _ptr(cpd)))
+        return "f32", er.value, ep.value, a, rpd, cpd
 
     def fused_solve(self, a, rpd, cpd, er, ep, tol, max_iter, workers=1) -> SolveOut:
         a = np.ascontiguousarray(a)

@@ -41,6 +41,9 @@ int guarded(F&& f) {
   } catch (const uot::PartitionError& e) {
     g_last_error = e.what();
     return 3;
+  } catch (const uot::IoError& e) {
+    g_last_error = e.what();
+    return 7;
   } catch (const std::exception& e) {
     g_last_error = e.what();
     return 9;
@@ -204,6 +207,37 @@ int ref_baseline_solve_f32(const float* a, std::size_t m, std::size_t n, const d
     *iterations = r.report.iterations;
     *final_error = r.report.final_error;
     *converged = r.report.converged ? 1 : 0;
+  });
+}
+
+// write_problem / read_problem (problem_io.cpp:97-141) of a Problem<float>.
+int ref_write_problem_f32(const char* path, const float* a, std::size_t m, std::size_t n, const double* rpd,
+                          const double* cpd, double er, double ep) {
+  return guarded([&] { uot::write_problem(path, uot::AnyProblem(make_problem(a, m, n, rpd, cpd, er, ep))); });
+}
+int ref_write_problem_f64(const char* path, const double* a, std::size_t m, std::size_t n, const double* rpd,
+                          const double* cpd, double er, double ep) {
+  return guarded([&] { uot::write_problem(path, uot::AnyProblem(make_problem(a, m, n, rpd, cpd, er, ep))); });
+}
+// Reads the header (m, n, dtype) and, when the buffers are given, the f32 payload.
+int ref_read_problem_f32(const char* path, std::size_t* m, std::size_t* n, int* dtype, double* er, double* ep,
+                         float* a, double* rpd, double* cpd) {
+  return guarded([&] {
+    const uot::AnyProblem any = uot::read_problem(path);
+    *m = uot::problem_rows(any);
+    *n = uot::problem_cols(any);
+    *dtype = uot::problem_dtype(any) == uot::Dtype::f32 ? 1 : 2;
+    if (const auto* p = std::get_if<uot::Problem<float>>(&any)) {
+      *er = p->er;
+      *ep = p->ep;
+      if (a) std::memcpy(a, p->a.data().data(), p->a.size() * sizeof(float));
+      if (rpd) std::memcpy(rpd, p->rpd.data(), p->rpd.size() * sizeof(double));
+      if (cpd) std::memcpy(cpd, p->cpd.data(), p->cpd.size() * sizeof(double));
+    } else {
+      const auto& q = std::get<uot::Problem<double>>(any);
+      *er = q.er;
+      *ep = q.ep;
+    }
   });
 }
 

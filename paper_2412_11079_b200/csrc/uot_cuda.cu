@@ -3,7 +3,10 @@
 // GPU (or one rank's row block of it), driven on one CUDA stream.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -245,6 +248,7 @@ struct uot_ctx {
   Control* h_ctl = nullptr;  // pinned mirror
 
   double fi = 0.0;
+  double er = 1.0, ep = 1.0;  // the Problem's coefficients (written back by uot_save_problem_file)
   bool have_problem = false, seeded = false;
 
   bool timing = false;
@@ -892,6 +896,8 @@ int uot_set_problem(uot_ctx* ctx, const float* a, const double* rpd, const doubl
   CK(cudaSetDevice(ctx->device));
   int rc = check_marginals(ctx, rpd, cpd, er, ep);
   if (rc) return rc;
+  ctx->er = er;
+  ctx->ep = ep;
   ctx->have_problem = false;
   CK(cudaMemcpy2DAsync(ctx->P, ctx->pitch * sizeof(float), a, ctx->cols * sizeof(float),
                        ctx->cols * sizeof(float), ctx->rows, cudaMemcpyHostToDevice, ctx->stream));
@@ -908,6 +914,8 @@ int uot_generate_problem(uot_ctx* ctx, uint64_t seed, double er, double ep) {
   CK(cudaSetDevice(ctx->device));
   if (uot_compute_fi(er, ep, &ctx->fi) != UOT_OK)
     return ctx->fail(UOT_INVALID_PARAMETER, "er must be positive and finite, ep non-negative and finite");
+  ctx->er = er;
+  ctx->ep = ep;
   ctx->have_problem = false;
   const unsigned gblocks = static_cast<unsigned>(ctx->sms) * 16;
   gen_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->P, seed, ctx->row_offset, ctx->rows,
@@ -1205,6 +1213,253 @@ int uot_gen_block_f32(uint64_t seed, uint64_t global_rows, uint64_t n, uint64_t 
 int uot_gen_problem_f32(uint64_t seed, uint64_t m, uint64_t n, float* a, double* rpd, double* cpd,
                         int threads) {
   return uot_gen_block_f32(seed, m, n, 0, m, a, rpd, cpd, threads);
+}
+
+}  // extern "C"
+
+// ==================================================== .uotp problem files ====
+// The reference's container (problem_io.cpp:13-141): 40-byte little-endian
+// header {"UOTP", u16 version 1, u16 dtype (1 f32, 2 f64), u64 M, u64 N, f64 er,
+// f64 ep}, then A row-major, rpd (M f64), cpd (N f64); the file size must equal
+// the header's extents exactly. Sessions stream THEIR row block between the file
+// and HBM through two page-locked staging buffers (read/write overlapped with
+// the copies), so a rank never materialises the global matrix on the host.
+namespace {
+
+thread_local std::string g_io_error;
+
+constexpr uint64_t kUotpHeader = 40;
+
+struct UotpHeader {
+  uint64_t m = 0, n = 0;
+  int dtype = 0;
+  double er = 0.0, ep = 0.0;
+  uint64_t elem = 4;
+};
+
+int io_fail(const std::string& msg) {
+  g_io_error = msg;
+  return UOT_IO_ERROR;
+}
+
+uint64_t get_le(const unsigned char* p, int bytes) {
+  uint64_t v = 0;
+  for (int k = bytes - 1; k >= 0; --k) v = (v << 8) | p[k];
+  return v;
+}
+void put_le(unsigned char* p, uint64_t v, int bytes) {
+  for (int k = 0; k < bytes; ++k) p[k] = static_cast<unsigned char>(v >> (8 * k));
+}
+
+// read_problem's checks in its order (problem_io.cpp:106-135); little-endian host.
+int read_uotp_header(int fd, const char* path, UotpHeader* h) {
+  struct stat st;
+  if (fstat(fd, &st) != 0) return io_fail(std::string("read_problem: cannot open ") + path);
+  const uint64_t size = static_cast<uint64_t>(st.st_size);
+  if (size < kUotpHeader) return io_fail("read_problem: truncated header");
+  unsigned char b[kUotpHeader];
+  if (pread(fd, b, kUotpHeader, 0) != static_cast<ssize_t>(kUotpHeader))
+    return io_fail(std::string("read_problem: short read from ") + path);
+  if (std::memcmp(b, "UOTP", 4) != 0) return io_fail("read_problem: bad magic");
+  const uint64_t version = get_le(b + 4, 2);
+  if (version != 1) return io_fail("read_problem: unsupported version " + std::to_string(version));
+  const uint64_t dtype = get_le(b + 6, 2);
+  if (dtype != 1 && dtype != 2) return io_fail("read_problem: unknown dtype code " + std::to_string(dtype));
+  h->m = get_le(b + 8, 8);
+  h->n = get_le(b + 16, 8);
+  if (h->m < 1 || h->n < 1) return io_fail("read_problem: matrix must be at least 1x1");
+  uint64_t er = get_le(b + 24, 8), ep = get_le(b + 32, 8);
+  std::memcpy(&h->er, &er, 8);
+  std::memcpy(&h->ep, &ep, 8);
+  h->dtype = static_cast<int>(dtype);
+  h->elem = dtype == 1 ? 4 : 8;
+  const unsigned __int128 expected = static_cast<unsigned __int128>(kUotpHeader) +
+                                     static_cast<unsigned __int128>(h->m) * h->n * h->elem +
+                                     static_cast<unsigned __int128>(8) * (h->m + h->n);
+  if (static_cast<unsigned __int128>(size) != expected)
+    return io_fail("read_problem: payload size does not match header extents");
+  return UOT_OK;
+}
+
+bool pread_all(int fd, void* buf, uint64_t bytes, uint64_t off) {
+  auto* p = static_cast<unsigned char*>(buf);
+  while (bytes) {
+    const ssize_t r = pread(fd, p, std::min<uint64_t>(bytes, 1ull << 30), static_cast<off_t>(off));
+    if (r <= 0) return false;
+    p += r;
+    off += static_cast<uint64_t>(r);
+    bytes -= static_cast<uint64_t>(r);
+  }
+  return true;
+}
+bool pwrite_all(int fd, const void* buf, uint64_t bytes, uint64_t off) {
+  auto* p = static_cast<const unsigned char*>(buf);
+  while (bytes) {
+    const ssize_t r = pwrite(fd, p, std::min<uint64_t>(bytes, 1ull << 30), static_cast<off_t>(off));
+    if (r <= 0) return false;
+    p += r;
+    off += static_cast<uint64_t>(r);
+    bytes -= static_cast<uint64_t>(r);
+  }
+  return true;
+}
+
+struct Fd {
+  int fd = -1;
+  ~Fd() {
+    if (fd >= 0) close(fd);
+  }
+};
+
+// Two page-locked staging buffers of whole rows: file <-> HBM, overlapped.
+struct Staging {
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  uint64_t rows_per = 0;
+  ~Staging() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev[i]) cudaEventDestroy(ev[i]);
+      if (buf[i]) cudaFreeHost(buf[i]);
+    }
+  }
+  int init(uot_ctx* ctx) {
+    const uint64_t row_bytes = ctx->cols * 4;
+    rows_per = std::max<uint64_t>(1, (64ull << 20) / row_bytes);
+    rows_per = std::min<uint64_t>(rows_per, ctx->rows);
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaMallocHost(&buf[i], rows_per * row_bytes));
+      CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    return UOT_OK;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* uot_last_io_error(void) { return g_io_error.c_str(); }
+
+int uot_problem_file_info(const char* path, uint64_t* m, uint64_t* n, int* dtype, double* er, double* ep) {
+  if (!path) return UOT_INVALID_PARAMETER;
+  Fd f;
+  f.fd = open(path, O_RDONLY);
+  if (f.fd < 0) return io_fail(std::string("read_problem: cannot open ") + path);
+  UotpHeader h;
+  const int rc = read_uotp_header(f.fd, path, &h);
+  if (rc) return rc;
+  if (m) *m = h.m;
+  if (n) *n = h.n;
+  if (dtype) *dtype = h.dtype;
+  if (er) *er = h.er;
+  if (ep) *ep = h.ep;
+  return UOT_OK;
+}
+
+int uot_load_problem_file(uot_ctx* ctx, const char* path) {
+  if (!ctx || !path) return UOT_INVALID_PARAMETER;
+  CK(cudaSetDevice(ctx->device));
+  Fd f;
+  f.fd = open(path, O_RDONLY);
+  if (f.fd < 0) return ctx->fail(UOT_IO_ERROR, "read_problem: cannot open %s", path);
+  UotpHeader h;
+  if (read_uotp_header(f.fd, path, &h)) return ctx->fail(UOT_IO_ERROR, "%s", g_io_error.c_str());
+  if (h.dtype != UOT_F32)
+    return ctx->fail(UOT_INVALID_PARAMETER, "%s holds a Problem<double>: only f32 has an sm_100a kernel", path);
+  if (h.m != ctx->global_rows || h.n != ctx->cols)
+    return ctx->fail(UOT_INVALID_PARAMETER, "%s is %llux%llu, the session expects %llux%llu", path,
+                     (unsigned long long)h.m, (unsigned long long)h.n, (unsigned long long)ctx->global_rows,
+                     (unsigned long long)ctx->cols);
+  const uint64_t mat_off = kUotpHeader, rpd_off = mat_off + h.m * h.n * 4, cpd_off = rpd_off + 8 * h.m;
+  std::vector<double> rpd(ctx->rows), cpd(ctx->cols);
+  if (!pread_all(f.fd, rpd.data(), 8 * ctx->rows, rpd_off + 8 * ctx->row_offset) ||
+      !pread_all(f.fd, cpd.data(), 8 * ctx->cols, cpd_off))
+    return ctx->fail(UOT_IO_ERROR, "read_problem: short read from %s", path);
+  int rc = check_marginals(ctx, rpd.data(), cpd.data(), h.er, h.ep);
+  if (rc) return rc;
+  ctx->er = h.er;
+  ctx->ep = h.ep;
+  ctx->have_problem = false;
+  Staging sg;
+  if ((rc = sg.init(ctx))) return rc;
+  const uint64_t row_bytes = ctx->cols * 4;
+  for (uint64_t r0 = 0, k = 0; r0 < ctx->rows; r0 += sg.rows_per, ++k) {
+    const uint64_t nr = std::min<uint64_t>(sg.rows_per, ctx->rows - r0);
+    const int i = static_cast<int>(k & 1);
+    CK(cudaEventSynchronize(sg.ev[i]));  // the copy out of this buffer two chunks ago is done
+    if (!pread_all(f.fd, sg.buf[i], nr * row_bytes, mat_off + (ctx->row_offset + r0) * row_bytes))
+      return ctx->fail(UOT_IO_ERROR, "read_problem: short read from %s", path);
+    CK(cudaMemcpy2DAsync(ctx->P + r0 * ctx->pitch, ctx->pitch * sizeof(float), sg.buf[i], row_bytes, row_bytes, nr,
+                         cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(sg.ev[i], ctx->stream));
+  }
+  CK(cudaMemcpyAsync(ctx->rpd, rpd.data(), ctx->rows * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->cpd, cpd.data(), ctx->cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if ((rc = reset_state(ctx))) return rc;
+  if ((rc = after_matrix_upload(ctx))) return rc;  // require_valid's matrix check (problem.hpp:64-98)
+  ctx->have_problem = true;
+  return UOT_OK;
+}
+
+int uot_save_problem_file(uot_ctx* ctx, const char* path) {
+  if (!ctx || !path) return UOT_INVALID_PARAMETER;
+  if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
+  CK(cudaSetDevice(ctx->device));
+  Fd f;
+  f.fd = open(path, O_WRONLY | O_CREAT, 0644);  // every rank opens; no truncation races
+  if (f.fd < 0) return ctx->fail(UOT_IO_ERROR, "write_problem: cannot open %s", path);
+  const uint64_t m = ctx->global_rows, n = ctx->cols;
+  const uint64_t mat_off = kUotpHeader, rpd_off = mat_off + m * n * 4, cpd_off = rpd_off + 8 * m;
+  if (ftruncate(f.fd, static_cast<off_t>(cpd_off + 8 * n)) != 0)
+    return ctx->fail(UOT_IO_ERROR, "write_problem: cannot size %s", path);
+  if (ctx->rank == 0) {
+    unsigned char b[kUotpHeader];
+    std::memcpy(b, "UOTP", 4);
+    put_le(b + 4, 1, 2);
+    put_le(b + 6, UOT_F32, 2);
+    put_le(b + 8, m, 8);
+    put_le(b + 16, n, 8);
+    uint64_t er, ep;
+    std::memcpy(&er, &ctx->er, 8);
+    std::memcpy(&ep, &ctx->ep, 8);
+    put_le(b + 24, er, 8);
+    put_le(b + 32, ep, 8);
+    std::vector<double> cpd(n);
+    CK(cudaMemcpyAsync(cpd.data(), ctx->cpd, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (!pwrite_all(f.fd, b, kUotpHeader, 0) || !pwrite_all(f.fd, cpd.data(), 8 * n, cpd_off))
+      return ctx->fail(UOT_IO_ERROR, "write_problem: short write to %s", path);
+  }
+  std::vector<double> rpd(ctx->rows);
+  CK(cudaMemcpyAsync(rpd.data(), ctx->rpd, ctx->rows * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  Staging sg;
+  int rc = sg.init(ctx);
+  if (rc) return rc;
+  const uint64_t row_bytes = n * 4;
+  uint64_t pend_r0[2] = {0, 0}, pend_nr[2] = {0, 0};
+  auto flush = [&](int i) -> bool {
+    if (!pend_nr[i]) return true;
+    if (cudaEventSynchronize(sg.ev[i]) != cudaSuccess) return false;
+    const bool ok = pwrite_all(f.fd, sg.buf[i], pend_nr[i] * row_bytes, mat_off + (ctx->row_offset + pend_r0[i]) * row_bytes);
+    pend_nr[i] = 0;
+    return ok;
+  };
+  for (uint64_t r0 = 0, k = 0; r0 < ctx->rows; r0 += sg.rows_per, ++k) {
+    const uint64_t nr = std::min<uint64_t>(sg.rows_per, ctx->rows - r0);
+    const int i = static_cast<int>(k & 1);
+    if (!flush(i)) return ctx->fail(UOT_IO_ERROR, "write_problem: short write to %s", path);
+    CK(cudaMemcpy2DAsync(sg.buf[i], row_bytes, ctx->P + r0 * ctx->pitch, ctx->pitch * sizeof(float), row_bytes, nr,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaEventRecord(sg.ev[i], ctx->stream));
+    pend_r0[i] = r0;
+    pend_nr[i] = nr;
+  }
+  if (!flush(0) || !flush(1)) return ctx->fail(UOT_IO_ERROR, "write_problem: short write to %s", path);
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (!pwrite_all(f.fd, rpd.data(), 8 * ctx->rows, rpd_off + 8 * ctx->row_offset))
+    return ctx->fail(UOT_IO_ERROR, "write_problem: short write to %s", path);
+  return UOT_OK;
 }
 
 }  // extern "C"

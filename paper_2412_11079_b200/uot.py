@@ -17,7 +17,9 @@ Names, argument meaning and errors follow /root/reference/proj/core/include/uot:
   fused_iterate               fused.hpp:164-191 / 197-250
   fused_solve                 fused.hpp:259-291
   Session                     (device-resident form of the loop above)
-  Error, InvalidParameter, DegenerateSum, ConfigError, PartitionError
+  read_problem / write_problem, Session.load_problem_file / save_problem_file
+                              problem_io.cpp:13-141 (.uotp)
+  Error, InvalidParameter, DegenerateSum, ConfigError, PartitionError, IoError
                               error.hpp:9-37
   ==========================  =============================================
 
@@ -62,12 +64,16 @@ class CudaError(Error):
     """CUDA / NCCL runtime failure (no reference analogue)."""
 
 
+class IoError(Error):
+    """uot::IoError (error.hpp:34-37): malformed or unreadable problem file."""
+
+
 class CudaExtensionMissing(ImportError):
     """The sm_100a extension is not built; there is deliberately no fallback."""
 
 
 _ERRORS = {1: InvalidParameter, 2: DegenerateSum, 3: PartitionError, 4: ConfigError,
-           5: CudaError, 6: CudaError}
+           5: CudaError, 6: CudaError, 7: IoError}
 
 UOT_F32, UOT_F64 = 1, 2
 
@@ -116,6 +122,11 @@ def lib():
     L.uot_peer_connect.argtypes = [_P, _P]
     L.uot_exchange_mode.argtypes = [_P]
     L.uot_set_variant.argtypes = [_P, _i]
+    L.uot_problem_file_info.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_i),
+                                        C.POINTER(_d), C.POINTER(_d)]
+    L.uot_last_io_error.restype = C.c_char_p
+    L.uot_load_problem_file.argtypes = [_P, C.c_char_p]
+    L.uot_save_problem_file.argtypes = [_P, C.c_char_p]
     L.uot_destroy.argtypes = [_P]
     L.uot_destroy.restype = None
     L.uot_last_error.argtypes = [_P]
@@ -299,6 +310,46 @@ def gen_problem_t(seed: int, m: int, n: int, threads: int = 0, out: np.ndarray |
     return Problem(a, rpd, cpd, 1.0, 1.0)
 
 
+# ---------------------------------------------------------- problem files --
+
+
+def problem_file_info(path) -> dict:
+    """The header of a .uotp file, with read_problem's checks (problem_io.cpp:106-135)."""
+    m, n, dt, er, ep = _u64(), _u64(), _i(), _d(), _d()
+    rc = lib().uot_problem_file_info(os.fsencode(path), C.byref(m), C.byref(n), C.byref(dt), C.byref(er),
+                                     C.byref(ep))
+    if rc:
+        _raise(rc, lib().uot_last_io_error().decode())
+    return {"m": int(m.value), "n": int(n.value), "dtype": {1: "f32", 2: "f64"}[dt.value],
+            "er": float(er.value), "ep": float(ep.value)}
+
+
+def read_problem(path) -> Problem:
+    """read_problem (problem_io.cpp:106-141) on the host for an f32 file."""
+    info = problem_file_info(path)
+    if info["dtype"] != "f32":
+        _raise(1, f"{path} holds a Problem<double>: only f32 has an sm_100a kernel")
+    m, n = info["m"], info["n"]
+    raw = np.fromfile(path, dtype=np.uint8, offset=40)
+    a = raw[: 4 * m * n].view("<f4").reshape(m, n)
+    rpd = raw[4 * m * n: 4 * m * n + 8 * m].view("<f8")
+    cpd = raw[4 * m * n + 8 * m:].view("<f8")
+    return Problem(a.astype(np.float32), rpd.astype(np.float64), cpd.astype(np.float64), info["er"], info["ep"])
+
+
+def write_problem(path, p: Problem):
+    """write_problem (problem_io.cpp:97-104) of a Problem<float> from host memory."""
+    a = np.ascontiguousarray(p.a, "<f4")
+    hdr = bytearray(b"UOTP") + (1).to_bytes(2, "little") + (1).to_bytes(2, "little")
+    hdr += int(a.shape[0]).to_bytes(8, "little") + int(a.shape[1]).to_bytes(8, "little")
+    hdr += np.array([p.er, p.ep], "<f8").tobytes()
+    with open(path, "wb") as f:
+        f.write(bytes(hdr))
+        f.write(a.tobytes())
+        f.write(np.ascontiguousarray(p.rpd, "<f8").tobytes())
+        f.write(np.ascontiguousarray(p.cpd, "<f8").tobytes())
+
+
 # ---------------------------------------------------------------- session --
 
 
@@ -375,6 +426,16 @@ class Session:
         if cpd.size != self.cols:
             _raise(1, f"column-marginal length {cpd.size} does not match column count {self.cols}")
         self._check(lib().uot_set_problem(self._h, _ptr(a), _ptr(rpd), _ptr(cpd), float(p.er), float(p.ep)))
+
+    def load_problem_file(self, path):
+        """read_problem (problem_io.cpp:106-141) of this session's row block,
+        streamed from the .uotp file straight to HBM, then validated."""
+        self._check(lib().uot_load_problem_file(self._h, os.fsencode(path)))
+
+    def save_problem_file(self, path):
+        """write_problem (problem_io.cpp:97-104) of the current plan with the
+        session's marginals and er/ep (collective over the ranks)."""
+        self._check(lib().uot_save_problem_file(self._h, os.fsencode(path)))
 
     def set_fi(self, fi: float):
         self._check(lib().uot_set_fi(self._h, float(fi)))

@@ -12,6 +12,8 @@ MODE
             alpha error) summed in ascending rank order — what the sessions do
             on device; checked against the oracle's distributed_solve.
   bytes     the host handshake helpers (all_gather_bytes / broadcast_bytes).
+  io        every rank streams its row block of a .uotp file into its session,
+            solves, and writes the plan back collectively (one shared file).
 Results go to OUT/rank{r}.npz (or .json).
 """
 from __future__ import annotations
@@ -39,6 +41,8 @@ def main():
             protocol(rank, world, out, *args)
         elif mode == "bytes":
             handshake(rank, world, out)
+        elif mode == "io":
+            io_roundtrip(rank, world, out, *args)
         else:
             raise SystemExit(f"unknown mode {mode}")
     finally:
@@ -94,6 +98,22 @@ def protocol(rank, world, out, seed, rows, cols, k, ep):
         cs = red[:cols]
         err = max(float(np.max(red[cols:])), float(np.max(np.abs(beta - 1.0))))
     np.savez(os.path.join(out, f"rank{rank}.npz"), plan=blk, alpha=alpha, beta=beta, err=err, b=b, e=e)
+
+
+def io_roundtrip(rank, world, out, k):
+    from paper_2412_11079_b200 import distributed as D
+    from paper_2412_11079_b200 import uot
+    src = os.environ["MR_UOTP"]
+    info = uot.problem_file_info(src)
+    s = D.make_session(info["m"], info["n"], int(os.environ.get("MR_DEVICE", "0")))
+    try:
+        s.load_problem_file(src)
+        s.init_col_sums()
+        it, err, conv = s.iterate(k, 1e-300)
+        s.save_problem_file(os.path.join(out, "plan.uotp"))
+        np.savez(os.path.join(out, f"rank{rank}.npz"), it=it, err=err, b=s.row_offset, e=s.row_offset + s.rows)
+    finally:
+        s.close()
 
 
 def handshake(rank, world, out):
