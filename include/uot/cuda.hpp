@@ -10,6 +10,10 @@
 //   uot::fused_solve(p, tol, max_iter, workers)   ->  uot::cuda::fused_solve(p, tol, max_iter)
 //   uot::fused_iterate(a, state, p, fi)           ->  uot::cuda::fused_iterate(a, state, p, fi)
 //   uot::distributed_solve(p, tol, max_iter, P)   ->  uot::cuda::distributed_solve(p, tol, max_iter, rank, P, nccl_id)
+//                                                     or uot::cuda::distributed_solve_peer(..., allgather)
+//   uot::baseline_solve(p, tol, max_iter)         ->  uot::cuda::baseline_solve(p, tol, max_iter)
+//   uot::tiled_solve(p, tol, max_iter, ...)       ->  uot::cuda::tiled_solve(p, tol, max_iter)
+//   uot::read_problem(path) + solve               ->  uot::cuda::load(path).iterate(...)
 //
 // plus uot::cuda::Session for loops that should keep the matrix resident in HBM
 // (the reference's per-iteration API moves the whole matrix every call).
@@ -17,9 +21,12 @@
 // uot/distributed.hpp) and link libuot_cuda.so. See INTEGRATION.md.
 #pragma once
 
+#include <array>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <filesystem>
+#include <functional>
 #include <span>
 #include <string>
 #include <utility>
@@ -40,6 +47,7 @@ namespace uot::cuda {
     case UOT_DEGENERATE_SUM: throw DegenerateSum(what);
     case UOT_PARTITION_ERROR: throw PartitionError(what);
     case UOT_CONFIG_ERROR: throw ConfigError(what);
+    case UOT_IO_ERROR: throw IoError(what);
     default: throw Error("cuda backend: " + what);
   }
 }
@@ -54,6 +62,23 @@ class Session {
   Session(std::size_t global_rows, std::size_t cols, int device, int rank, int nranks,
           const std::uint8_t* nccl_id) {
     check(uot_create_dist(&ctx_, global_rows, cols, UOT_F32, device, rank, nranks, nccl_id));
+  }
+  // Rank `rank` of `nranks` whose per-iteration allreduce is fused into the
+  // finalize kernels over peer memory (CUDA IPC over NVLink): connect() with
+  // every rank's peer_handle() before use (uot_create_peer, include/uot_cuda.h).
+  struct Peer {};
+  Session(std::size_t global_rows, std::size_t cols, int device, int rank, int nranks, Peer) {
+    check(uot_create_peer(&ctx_, global_rows, cols, UOT_F32, device, rank, nranks));
+  }
+  std::array<std::uint8_t, 64> peer_handle() const {
+    std::array<std::uint8_t, 64> h{};
+    check(uot_peer_handle(ctx_, h.data()));
+    return h;
+  }
+  void connect(const std::vector<std::array<std::uint8_t, 64>>& handles) {
+    std::vector<std::uint8_t> flat;
+    for (const auto& h : handles) flat.insert(flat.end(), h.begin(), h.end());
+    check(uot_peer_connect(ctx_, flat.data()));
   }
   Session(const Session&) = delete;
   Session& operator=(const Session&) = delete;
@@ -73,6 +98,14 @@ class Session {
     check(uot_set_problem(ctx_, p.a.data().data(), p.rpd.data(), p.cpd.data(), p.er, p.ep));
   }
   void set_fi(double fi) { check(uot_set_fi(ctx_, fi)); }
+  // read_problem / write_problem (problem_io.cpp:97-141) of this session's rows,
+  // streamed between the .uotp file and HBM.
+  void load_problem_file(const std::filesystem::path& path) { check(uot_load_problem_file(ctx_, path.c_str())); }
+  void save_problem_file(const std::filesystem::path& path) const {
+    check(uot_save_problem_file(ctx_, path.c_str()));
+  }
+  // UOT_VARIANT_FUSED (default), UOT_VARIANT_TWO_PASS (tiled.hpp), UOT_VARIANT_BASELINE (baseline.hpp).
+  void set_variant(int variant) { check(uot_set_variant(ctx_, variant)); }
   void set_plan(const Matrix<float>& a) { check(uot_set_plan(ctx_, a.data().data())); }
   void init_col_sums() { check(uot_init_col_sums(ctx_)); }
   void set_state(const FusedState& st) { check(uot_set_col_sums(ctx_, st.col_sums.data())); }
@@ -148,6 +181,56 @@ inline SolveResult<float> fused_solve(const Problem<float>& p, double tol, std::
   return r;
 }
 
+namespace detail {
+inline SolveResult<float> solve_with(const Problem<float>& p, double tol, std::size_t max_iter, int device,
+                                     int variant, const char* solver, const char* who) {
+  require_valid(p);
+  if (!(tol > 0.0)) throw InvalidParameter(std::string(who) + ": tol must be positive");
+  if (max_iter < 1) throw InvalidParameter(std::string(who) + ": max_iter must be at least 1");
+  const auto t0 = std::chrono::steady_clock::now();
+  Session s(p.m(), p.n(), device);
+  s.set_problem(p);
+  s.init_col_sums();
+  s.set_variant(variant);
+  const auto pr = s.iterate(max_iter, tol);
+  SolveResult<float> r;
+  r.plan = s.plan();
+  r.factors = s.factors();
+  r.report.solver = solver;
+  r.report.iterations = pr.iterations;
+  r.report.final_error = pr.final_error;
+  r.report.converged = pr.converged;
+  r.report.wall_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return r;
+}
+}  // namespace detail
+
+// baseline_solve (baseline.hpp:118-142): the four-sweep schedule on the GPU
+// (an ablation of the fused sweep: 3x its HBM traffic).
+inline SolveResult<float> baseline_solve(const Problem<float>& p, double tol, std::size_t max_iter,
+                                         int device = 0) {
+  return detail::solve_with(p, tol, max_iter, device, UOT_VARIANT_BASELINE, "baseline", "baseline_solve");
+}
+
+// tiled_solve (tiled.hpp:231-260): the paper's two-pass GPU data flow (part4 ->
+// row factors -> part2); the reference's TileConfig shapes have no meaning here.
+inline SolveResult<float> tiled_solve(const Problem<float>& p, double tol, std::size_t max_iter, int device = 0) {
+  return detail::solve_with(p, tol, max_iter, device, UOT_VARIANT_TWO_PASS, "tiled", "tiled_solve");
+}
+
+// A session holding the problem of a .uotp file (read_problem, problem_io.cpp:106-141).
+inline Session load(const std::filesystem::path& path, int device = 0) {
+  std::uint64_t m = 0, n = 0;
+  int dtype = 0;
+  double er = 0, ep = 0;
+  const int rc = uot_problem_file_info(path.c_str(), &m, &n, &dtype, &er, &ep);
+  if (rc != UOT_OK) raise(rc, uot_last_io_error());
+  Session s(m, n, device);
+  s.load_problem_file(path);
+  return s;
+}
+
 // fused_iterate (fused.hpp:164-191): `a` and `state` updated in place. Moves
 // the matrix over PCIe twice per call; prefer Session for loops.
 inline ScalingFactors fused_iterate(Matrix<float>& a, FusedState& state, const Problem<float>& p,
@@ -184,6 +267,43 @@ inline DistributedResult<float> distributed_solve(const Problem<float>& p, doubl
   if (max_iter < 1) throw InvalidParameter("distributed_solve: max_iter must be at least 1");
   const auto t0 = std::chrono::steady_clock::now();
   Session s(p.m(), p.n(), device, rank, nranks, nccl_id);
+  const auto lay = s.layout();
+  Problem<float> local;
+  local.a = Matrix<float>(lay.rows, p.n());
+  std::memcpy(local.a.data().data(), p.a.row(lay.row_offset), lay.rows * p.n() * sizeof(float));
+  local.rpd.assign(p.rpd.begin() + lay.row_offset, p.rpd.begin() + lay.row_offset + lay.rows);
+  local.cpd = p.cpd;
+  local.er = p.er;
+  local.ep = p.ep;
+  s.set_problem(local);
+  s.init_col_sums();
+  const auto pr = s.iterate(max_iter, tol);
+  DistributedResult<float> r;
+  r.plan = s.plan();
+  r.factors = s.factors();
+  r.comm = s.comm();
+  r.report.solver = "dist";
+  r.report.iterations = pr.iterations;
+  r.report.final_error = pr.final_error;
+  r.report.converged = pr.converged;
+  r.report.wall_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return r;
+}
+
+// distributed_solve with the column-sum allreduce fused into the finalize
+// kernels over peer memory: `allgather` is the caller's transport (MPI,
+// torch.distributed, a shared file, ...) and must return every rank's 64-byte
+// handle in rank order.
+using AllGather = std::function<std::vector<std::array<std::uint8_t, 64>>(const std::array<std::uint8_t, 64>&)>;
+inline DistributedResult<float> distributed_solve_peer(const Problem<float>& p, double tol, std::size_t max_iter,
+                                                       int rank, int nranks, int device, const AllGather& allgather) {
+  require_valid(p);
+  if (!(tol > 0.0)) throw InvalidParameter("distributed_solve: tol must be positive");
+  if (max_iter < 1) throw InvalidParameter("distributed_solve: max_iter must be at least 1");
+  const auto t0 = std::chrono::steady_clock::now();
+  Session s(p.m(), p.n(), device, rank, nranks, Session::Peer{});
+  if (nranks > 1) s.connect(allgather(s.peer_handle()));
   const auto lay = s.layout();
   Problem<float> local;
   local.a = Matrix<float>(lay.rows, p.n());

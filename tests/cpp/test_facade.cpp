@@ -10,9 +10,11 @@
 #include <string>
 #include <vector>
 
+#include "uot/baseline.hpp"
 #include "uot/cuda.hpp"
 #include "uot/fused.hpp"
 #include "uot/problem_io.hpp"
+#include "uot/tiled.hpp"
 
 namespace {
 
@@ -149,6 +151,47 @@ void test_single_rank_distributed() {  // test_distributed.cpp:92-104, 142-155
   CHECK(max_rel(d.plan, ref.plan) <= 1e-5);
 }
 
+void test_ablation_solvers_match_reference() {  // baseline.hpp:118-142, tiled.hpp
+  const auto p = random_problem(9, 200, 300, 0.5);
+  const auto rb = uot::baseline_solve(p, kNever, 12);
+  const auto gb = uot::cuda::baseline_solve(p, kNever, 12);
+  CHECK(gb.report.iterations == 12 && gb.report.solver == "baseline");
+  CHECK(max_rel(gb.plan, rb.plan) <= 1e-5);
+  CHECK(std::abs(gb.report.final_error - rb.report.final_error) <= 1e-9 * rb.report.final_error);
+  const auto rt = uot::tiled_solve(p, kNever, 12, uot::default_part2_config(200, 300), uot::default_part4_config(200, 300));
+  const auto gt = uot::cuda::tiled_solve(p, kNever, 12);
+  CHECK(max_rel(gt.plan, rt.plan) <= 1e-5);
+}
+
+void test_problem_files_round_trip() {  // problem_io.cpp:97-141
+  const auto p = random_problem(13, 40, 70, 0.5);
+  const std::filesystem::path in = std::filesystem::temp_directory_path() / "uot_facade_in.uotp";
+  const std::filesystem::path out = std::filesystem::temp_directory_path() / "uot_facade_out.uotp";
+  uot::write_problem(in, uot::AnyProblem(p));
+  auto s = uot::cuda::load(in);
+  CHECK(s.plan() == p.a);
+  s.init_col_sums();
+  s.iterate(5);
+  s.save_problem_file(out);
+  const auto back = std::get<uot::Problem<float>>(uot::read_problem(out));
+  const auto ref = uot::fused_solve(p, kNever, 5);
+  CHECK(max_rel(back.a, ref.plan) <= 1e-5);
+  CHECK(back.rpd == p.rpd && back.cpd == p.cpd && back.er == p.er && back.ep == p.ep);
+  CHECK_THROWS_AS(uot::cuda::load("/nonexistent/uot/path.uotp"), uot::IoError);
+  std::filesystem::remove(in);
+  std::filesystem::remove(out);
+}
+
+void test_single_rank_peer_distributed() {
+  const auto p = random_problem(25, 64, 64, 0.5);
+  const auto d = uot::cuda::distributed_solve_peer(p, kNever, 11, 0, 1, 0,
+                                                   [](const std::array<std::uint8_t, 64>& h) {
+                                                     return std::vector<std::array<std::uint8_t, 64>>{h};
+                                                   });
+  const auto ref = uot::distributed_solve(p, kNever, 11, std::size_t(1));
+  CHECK(d.report.iterations == 11 && max_rel(d.plan, ref.plan) <= 1e-5);
+}
+
 }  // namespace
 
 int main() {
@@ -159,6 +202,9 @@ int main() {
       {"session resumable + converges", test_session_is_resumable_and_converges},
       {"errors", test_errors_map_to_reference_exceptions},
       {"single-rank distributed", test_single_rank_distributed},
+      {"ablation solvers", test_ablation_solvers_match_reference},
+      {"problem files", test_problem_files_round_trip},
+      {"single-rank peer distributed", test_single_rank_peer_distributed},
   };
   for (const auto& [name, fn] : cases) {
     const int before = g_fail;
