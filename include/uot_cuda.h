@@ -69,6 +69,7 @@ typedef struct uot_layout {
   int32_t exchange;      /* 0 single GPU, 1 NCCL allreduce, 2 fused peer-memory exchange */
   int32_t tmem;          /* iterations park the alpha-lag rows in Tensor Memory (sweep_tmem.cuh) */
   int32_t resident;      /* uot_iterate runs as ONE persistent launch, matrix in shared memory (resident.cuh) */
+  int32_t persist;       /* otherwise, single rank: ONE persistent streaming launch (persist.cuh) */
 } uot_layout;
 
 /* ---- sessions ---------------------------------------------------------- */

@@ -50,14 +50,6 @@ struct ResidentArgs {
 // thread t of every CTA waits for flag t (acquire) — one L2 round trip after
 // the last arrival instead of nblocks serialised atomics on one address.
 // Epochs grow monotonically across launches (Control::bar_gen).
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 #ifdef UOT_FLAG_BARRIER
 __device__ __forceinline__ void grid_barrier(unsigned* flags, Control*, unsigned nblocks, unsigned epoch) {
   __syncthreads();

@@ -70,58 +70,42 @@ __device__ __forceinline__ float4 tmem_ld4(uint32_t taddr) {
 }
 
 // ---------------------------------------------------- per-row bodies --
-// fused.hpp:125-131: x1 = f32(f64(x0)*beta_j) from the load slot into TMEM
-// columns [tcol, tcol + 4V) of this thread's lane; returns the f64 row partial.
+// The arithmetic of sweep.cuh's bodies (window screen certifying x0 and x1,
+// two-op widening, hardware widening for the column sums); only where x1 waits
+// differs: TMEM columns [tcol, tcol + 4V) of this thread's lane.
+
+// fused.hpp:125-131: x1 = f32(f64(x0)*beta_j) from the load slot into TMEM;
+// returns the f64 row partial; `bad` when a group took the exact path.
 template <int NT, int V, bool FULL>
 __device__ __forceinline__ double row_sweep1_t(const float4* row, uint32_t tcol, unsigned tid, unsigned nq,
-                                               const double* beta, bool& x1bad) {
+                                               const double* beta, ScreenBounds sb, bool& bad) {
   constexpr int KG = ChunkGroup<V>::KG;
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  double s[4];
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
     float4 v[KG];
-    uint32_t m = 0;
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      const unsigned q = tid + (g0 + kk) * NT;
-      v[kk] = (FULL || q < nq) ? row[q] : make_float4(1.f, 1.f, 1.f, 1.f);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) m = nn_max(m, comp(v[kk], e));
-    }
-    if (nn_ok(m)) {
+    load_group<NT, KG, FULL>(row, v, g0, tid, nq);
+    const uint32_t m = screen_group<KG>(v, sb.lo);
+    double t[4];
+    if (m <= sb.span) {
 #pragma unroll
       for (int kk = 0; kk < KG; ++kk)
 #pragma unroll
         for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(fastd(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) t[e] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KG; ++kk)
+        if (FULL || tid + (g0 + kk) * NT < nq)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) t[e] += fastd(comp(v[kk], e));
     } else {
+      bad = true;
 #pragma unroll
       for (int kk = 0; kk < KG; ++kk)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           comp(v[kk], e) = d2f(static_cast<double>(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
-    }
-    __syncwarp();  // tcgen05.st is warp-collective (.sync.aligned)
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) tmem_st4(tcol + 4 * (g0 + kk), v[kk]);
-    uint32_t m1 = 0;
-    double t[4];
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      const unsigned q = tid + (g0 + kk) * NT;
-      if (FULL || q < nq) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          m1 = nn_max(m1, comp(v[kk], e));
-          const double x = fastd(comp(v[kk], e));
-          t[e] = kk == 0 ? x : t[e] + x;
-        }
-      } else if (kk == 0) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) t[e] = 0.0;
-      }
-    }
-    if (!nn_ok(m1)) {
-      x1bad = true;
 #pragma unroll
       for (int e = 0; e < 4; ++e) t[e] = 0.0;
 #pragma unroll
@@ -130,6 +114,9 @@ __device__ __forceinline__ double row_sweep1_t(const float4* row, uint32_t tcol,
 #pragma unroll
           for (int e = 0; e < 4; ++e) t[e] += static_cast<double>(comp(v[kk], e));
     }
+    __syncwarp();  // tcgen05.st is warp-collective (.sync.aligned)
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) tmem_st4(tcol + 4 * (g0 + kk), v[kk]);
 #pragma unroll
     for (int e = 0; e < 4; ++e) s[e] = g0 == 0 ? t[e] : s[e] + t[e];
   }
@@ -140,7 +127,7 @@ __device__ __forceinline__ double row_sweep1_t(const float4* row, uint32_t tcol,
 // next_j += f64(x2).
 template <int NT, int V, bool FULL>
 __device__ __forceinline__ void row_sweep2_t(uint32_t tcol, float4* out, unsigned tid, unsigned nq, double al,
-                                             bool x1bad, double* acc) {
+                                             bool exact, double* acc) {
   constexpr int KG = ChunkGroup<V>::KG;
   float4 v[V];
 #pragma unroll
@@ -148,40 +135,11 @@ __device__ __forceinline__ void row_sweep2_t(uint32_t tcol, float4* out, unsigne
   tmem_wait_ld();
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
-    if (!x1bad) {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) comp(v[g0 + kk], e) = d2f(fastd(comp(v[g0 + kk], e)) * al);
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) comp(v[g0 + kk], e) = d2f(static_cast<double>(comp(v[g0 + kk], e)) * al);
-    }
-    uint32_t m2 = 0;
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      const unsigned q = tid + (g0 + kk) * NT;
-      if (FULL || q < nq) {
-        out[q] = v[g0 + kk];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) m2 = nn_max(m2, comp(v[g0 + kk], e));
-      }
-    }
-    if (nn_ok(m2)) {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-        if (FULL || tid + (g0 + kk) * NT < nq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += fastd(comp(v[g0 + kk], e));
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk)
-        if (FULL || tid + (g0 + kk) * NT < nq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(v[g0 + kk], e));
-    }
+    float4 (&w)[KG] = *reinterpret_cast<float4(*)[KG]>(&v[g0]);
+    if (exact)
+      group_sweep2<NT, KG, FULL, true>(out, w, g0, tid, nq, al, acc);
+    else
+      group_sweep2<NT, KG, FULL, false>(out, w, g0, tid, nq, al, acc);
   }
 }
 
@@ -417,6 +375,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_tmem_kernel(const
       for (int e = 0; e < 4; ++e) beta[4 * k + e] = (FULL || q < nq) ? bsrc[4 * q + e] : 1.0;
     }
   }
+  const ScreenBounds sb = screen_bounds(beta, 4 * V);
   // TMEM address of (batch slot, row r) for this thread: lane quarter warp%4,
   // column block (warp/4) within the slot.
   const uint32_t tlane = static_cast<uint32_t>(32 * (warp & 3)) << 16;
@@ -439,7 +398,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_tmem_kernel(const
         if (r < static_cast<int>(nr)) {
           bool bad = false;
           part[r] = row_sweep1_t<NT, V, FULL>(reinterpret_cast<const float4*>(buf + r * a.slice), tcol(s, r), tid,
-                                              nq, beta, bad);
+                                              nq, beta, sb, bad);
           if (bad) x1bad |= 1ull << (shift + r);
         }
       }

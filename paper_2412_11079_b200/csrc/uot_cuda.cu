@@ -25,6 +25,7 @@
 #include "sweep_tmem.cuh"
 #include "resident.cuh"
 #include "ablation.cuh"
+#include "persist.cuh"
 
 using namespace uotk;
 
@@ -41,6 +42,7 @@ struct SweepCfg {
   SweepFn iter[2];     // [FULL] smem-ring iteration kernel (sweep.cuh)
   SweepFn seed[2];     // [FULL]
   SweepFn iter_tm[2];  // [FULL] TMEM-lag iteration kernel (sweep_tmem.cuh)
+  void (*persist[2])(const PersistArgs);  // [FULL] K iterations per launch (persist.cuh)
   int la_tm;
   size_t (*smem_bytes)(unsigned buf_stride);
   size_t (*smem_bytes_tm)(unsigned buf_stride);
@@ -96,6 +98,8 @@ SweepCfg make_cfg() {
   c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true>;
   c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
+  c.persist[0] = persist_kernel<NT, V, BM, NB, LA, XCHG, NF, false>;
+  c.persist[1] = persist_kernel<NT, V, BM, NB, LA, XCHG, NF, true>;
   static_assert(UOT_TM_NL + UOT_TM_NS == NB, "TMEM kernel rings use the same shared memory");
   constexpr int LAT = XCHG ? UOT_TM_LA_X : UOT_TM_LA_G1;
   c.la_tm = LAT;
@@ -232,6 +236,7 @@ struct uot_ctx {
   size_t rsmem = 0;
   int rfull = 0;
   bool use_tmem = false;  // iterations run sweep_tmem_kernel (opt-in: UOT_TMEM=1)
+  bool use_persist = false;  // uot_iterate is one persistent streaming launch (persist.cuh, opt-in)
 
   // device buffers
   float* P = nullptr;
@@ -354,6 +359,17 @@ int plan_layout(uot_ctx* ctx) {
   if (ctx->use_tmem)
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(cfg->iter_tm[ctx->full]),
                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_tm)));
+  // Persistent streaming mode (persist.cuh, opt-in UOT_PERSIST=1): single rank,
+  // the smem-ring kernel. Measured 2-6% slower per iteration than sweep +
+  // finalize (its loop body spills under the 96-register cap), so off by default.
+  // Every CTA must stream more than NBUF batches per iteration: the producer then
+  // never prefetches a row batch before its previous-iteration store was issued.
+  const uint64_t nb_min = (ctx->rows / ctx->groups) / ctx->B;
+  ctx->use_persist = ctx->nranks == 1 && !ctx->use_tmem && env_int("UOT_PERSIST", 0) != 0 &&
+                     ctx->groups <= 160 && nb_min > static_cast<uint64_t>(cfg->nbuf);
+  if (ctx->use_persist)
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(cfg->persist[ctx->full]),
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem)));
   // Resident mode (resident.cuh): one rank, rows fit one CTA (G == 1), a CTA's
   // row block fits shared memory and at most 32 rows per CTA. UOT_RESIDENT=0: off.
   ctx->rcfg = nullptr;
@@ -539,6 +555,31 @@ int launch_ablation_iteration(uot_ctx* ctx) {
     ctx->launches += 6;
   }
   return ctx->cuda(cudaGetLastError(), "ablation launch");
+}
+
+// The whole iterate(k) call as one persistent streaming launch (persist.cuh).
+int launch_persist(uot_ctx* ctx, uint64_t k) {
+  PersistArgs p;
+  p.s = sweep_args(ctx);
+  p.cpd = ctx->cpd;
+  p.beta2w = ctx->beta2;
+  p.col_sums = ctx->col_sums;
+  p.bar = ctx->bar_flags;
+  p.cols = static_cast<unsigned>(ctx->cols);
+  p.grid = ctx->grid;
+  p.k = static_cast<unsigned>(std::min<uint64_t>(k, 0xffffffffu));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(ctx->grid);
+  lc.blockDim = dim3(ctx->cfg->nt + 32 * (1 + ctx->cfg->nf));
+  lc.dynamicSmemBytes = ctx->smem;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers + exchange need every CTA resident
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  ctx->launches++;
+  return ctx->cuda(cudaLaunchKernelEx(&lc, ctx->cfg->persist[ctx->full], p), "persistent sweep launch");
 }
 
 // The whole iterate(k) call as one cooperative launch (resident.cuh).
@@ -877,6 +918,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->smem_bytes = static_cast<uint32_t>(ctx->use_tmem ? ctx->smem_tm : ctx->smem);
   o->tmem = ctx->use_tmem ? 1 : 0;
   o->resident = ctx->rcfg ? 1 : 0;
+  o->persist = ctx->use_persist ? 1 : 0;
   o->nbuf = ctx->cfg->nbuf;
   o->sms = ctx->sms;
   o->rank = ctx->rank;
@@ -1022,6 +1064,10 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
   CK(cudaGetLastError());
   int rc;
   const bool resident = ctx->rcfg != nullptr && ctx->variant == UOT_VARIANT_FUSED;
+  // 32-bit global batch indices inside the persistent kernel: long calls are split
+  const uint64_t nb_max = (ctx->rows + ctx->groups - 1) / ctx->groups / ctx->B + 1;
+  const uint64_t kchunk = std::max<uint64_t>(
+      1, std::min<uint64_t>((1ull << 30) / nb_max, static_cast<uint64_t>(env_int("UOT_PERSIST_CHUNK", 1 << 30))));
   if (ctx->variant != UOT_VARIANT_FUSED) {
     for (uint64_t i = 0; i < k; ++i) {
       if (ctx->timing) record(ctx, 3 * i);
@@ -1029,9 +1075,14 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
       if (ctx->timing) record(ctx, 3 * i + 1);
       if (ctx->timing) record(ctx, 3 * i + 2);
     }
-  } else if (resident) {  // k iterations, one launch: sweep + reduction + stop test inside
+  } else if (resident || ctx->use_persist) {  // k iterations, one launch: sweeps, reductions, stop test inside
     if (ctx->timing) record(ctx, 0);
-    if ((rc = launch_resident(ctx, k))) return rc;
+    if (resident) {
+      if ((rc = launch_resident(ctx, k))) return rc;
+    } else {
+      for (uint64_t done = 0; done < k; done += kchunk)
+        if ((rc = launch_persist(ctx, std::min(kchunk, k - done)))) return rc;
+    }
     if (ctx->timing) record(ctx, 1);
   } else {
     for (uint64_t i = 0; i < k; ++i) {
@@ -1053,19 +1104,19 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
   }
   if (ctx->timing) {
     ctx->sweep_ms = ctx->fin_ms = 0.0;
-    if (resident) {  // one launch: reported as sweep time, no separate finalize
+    if (resident || ctx->use_persist) {  // one launch: reported as sweep time, no separate finalize
       float a = 0.f;
       cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
       ctx->sweep_ms = a;
     }
-    for (uint64_t i = 0; i < (resident ? 0 : k); ++i) {
+    for (uint64_t i = 0; i < ((resident || ctx->use_persist) ? 0 : k); ++i) {
       float a = 0.f, b = 0.f;
       cudaEventElapsedTime(&a, ctx->ev[3 * i], ctx->ev[3 * i + 1]);
       cudaEventElapsedTime(&b, ctx->ev[3 * i + 1], ctx->ev[3 * i + 2]);
       ctx->sweep_ms += a;
       ctx->fin_ms += b;
     }
-    ctx->sweeps_timed = resident ? std::max<uint64_t>(1, ctx->h_ctl->iter - before) : k;
+    ctx->sweeps_timed = (resident || ctx->use_persist) ? std::max<uint64_t>(1, ctx->h_ctl->iter - before) : k;
   }
   if (iterations) *iterations = ctx->h_ctl->iter - before;
   if (final_error) *final_error = ctx->h_ctl->last_error;

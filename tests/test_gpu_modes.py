@@ -5,7 +5,9 @@
 * resident: the whole call is ONE cooperative launch with the matrix in shared
   memory and two grid barriers per iteration (resident.cuh) — small shapes;
 * TMEM lag (opt-in): the streaming sweep with the alpha lag parked in Tensor
-  Memory (sweep_tmem.cuh).
+  Memory (sweep_tmem.cuh);
+* persistent streaming (opt-in): all k iterations in one launch of the ring
+  kernel, the finalize replaced by grid barriers (persist.cuh).
 
 Each mode is checked against the CPU oracle (fused_solve, fused.hpp:259-291)
 and the modes against each other, including the early exit and the
@@ -102,3 +104,29 @@ def test_tmem_lag_variant_matches_oracle(gpu, orc, m, n, k):
     assert lay["tmem"] == 1 and it == k
     assert_parity(plan, ref.plan, rpd, cpd, f"tmem {m}x{n}")
     np.testing.assert_allclose(f.alpha, ref.alpha, rtol=1e-12)
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 4096, 9), (1500, 20000, 6), (3000, 4096, 12)])
+def test_persistent_streaming_matches_oracle(gpu, orc, m, n, k):
+    a, rpd, cpd = orc.gen_problem(42, m, n)
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 8)
+    env = {"UOT_PERSIST": "1", "UOT_RESIDENT": "0"}
+    plan, f, cs, it, err, conv, lay = run(gpu, a, rpd, cpd, 1.0, 0.1, k, env=env)
+    assert lay["persist"] == 1 and it == k
+    assert_parity(plan, ref.plan, rpd, cpd, f"persist {m}x{n}")
+    # f64 sums in another order can flip the last bit of a stored f32 entry,
+    # which moves that column's sum by ~ulp(x)/rows
+    np.testing.assert_allclose(f.alpha, ref.alpha, rtol=1e-10)
+    np.testing.assert_allclose(cs, ref.col_sums, rtol=1e-8)
+    assert abs(err - ref.final_error) <= 1e-9 * max(1.0, ref.final_error)
+    split = run(gpu, a, rpd, cpd, 1.0, 0.1, k, env=env, chunks=[2, k - 2])
+    assert np.array_equal(split[0], plan)
+
+
+def test_persistent_streaming_early_exit(gpu, orc):
+    a, rpd, cpd = orc.gen_problem(5, 6000, 2048)
+    cpd = cpd * (rpd.sum() / cpd.sum())
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.0, 1e-6, 10000, 1)
+    r = run(gpu, a, rpd, cpd, 1.0, 0.0, 10000, tol=1e-6, env={"UOT_PERSIST": "1", "UOT_RESIDENT": "0"})
+    assert r[6]["persist"] == 1 and ref.converged and r[5] and r[3] == ref.iterations
+    assert_parity(r[0], ref.plan, rpd, cpd, "persist converged")

@@ -21,5 +21,5 @@ for spec in sys.argv[1:]:
         gbs = 2 * m * n * 4 / (sw / n_ * 1e-3) / 1e9
         lay = s.layout
         print(f"[{tag}] {m}x{n}: sweep {sw / n_ * 1e3:.1f} us ({gbs:.0f} GB/s) finalize {fin / n_ * 1e3:.1f} us "
-              f"G={lay["G"]} res={lay["resident"]} tm={lay["tmem"]} smid={lay["smid_map"]} groups={lay["groups"]} B={lay['rows_per_step']} thr={lay['threads']} v={lay['chunks']}",
+              f"G={lay["G"]} per={lay["persist"]} res={lay["resident"]} tm={lay["tmem"]} smid={lay["smid_map"]} groups={lay["groups"]} B={lay['rows_per_step']} thr={lay['threads']} v={lay['chunks']}",
               flush=True)
