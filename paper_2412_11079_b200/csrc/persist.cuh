@@ -214,33 +214,9 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) persist_kernel(const Pe
 #pragma unroll
           for (int w = 1; w < NW; ++w) t += red[(q * NW + w) * BM + lane];
         }
-        if (XCHG) {  // as sweep.cuh: {partial, tag} records in L2, ascending-g sum
-          if (lane == 0)
-            st_relaxed_b128(&a.xrec[static_cast<size_t>(cta) * kRing + (gs % kRing)],
-                            static_cast<unsigned long long>(__double_as_longlong(t)), tag_hi | (s + 1));
-          double v = 0.0;
-          if (lane < static_cast<int>(G)) {
-            const ulonglong2* rec = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (gs % kRing)];
-            const unsigned long long want = tag_hi | (s + 1);
-            unsigned long long lo, hi;
-            ld_relaxed_b128(rec, lo, hi);
-            if (hi != want) {
-              const unsigned long long tt0 = globaltimer_ns();
-              unsigned n = 0;
-              do {
-                ld_relaxed_b128(rec, lo, hi);
-                if (hi != want && (++n & 255u) == 0 && globaltimer_ns() - tt0 > kExchangeTimeoutNs) {
-                  atomicOr(&ctl->status, kStatusExchangeTimeout);
-                  break;
-                }
-              } while (hi != want);
-            }
-            v = __longlong_as_double(static_cast<long long>(lo));
-          }
-          double tot = 0.0;
-          for (unsigned k = 0; k < G; ++k) tot += __shfl_sync(0xffffffffu, v, k);
-          t = tot;
-        }
+        if (XCHG)  // as sweep.cuh: {partial, tag} records in L2, ascending-g sum
+          t = exchange_row_sum(a.xrec, cta, group, G, gs % kRing, tag_hi | (s + 1), t, ctl);
+
         if (lane < static_cast<int>(nr)) {
           double al;
           if (!rescale_factor_dev(rv, t, a.fi, &al)) {

@@ -98,6 +98,43 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;  // xor tree: every lane holds the bit-identical total (fp add commutes)
 }
 
+// Row-sum exchange of a G-CTA row group (G > 1): publish this CTA's partial of
+// the row as a 128-bit single-copy-atomic {value, tag} record in L2 (no
+// fences), then gather the G records of the row — one lane per record, 32 at a
+// time, spinning on L2 (any back-off costs more than the polls) — and add them
+// in ascending g: identical bits on every CTA of the group. Whole warp calls.
+__device__ __forceinline__ double exchange_row_sum(ulonglong2* xrec, unsigned cta, unsigned group, unsigned G,
+                                                   unsigned slot, unsigned long long tag, double t, Control* ctl) {
+  const unsigned lane = threadIdx.x & 31;
+  if (lane == 0)
+    st_relaxed_b128(&xrec[static_cast<size_t>(cta) * kRing + slot],
+                    static_cast<unsigned long long>(__double_as_longlong(t)), tag);
+  double tot = 0.0;
+  for (unsigned g0 = 0; g0 < G; g0 += 32) {
+    double v = 0.0;
+    if (g0 + lane < G) {
+      const ulonglong2* rec = &xrec[static_cast<size_t>(group * G + g0 + lane) * kRing + slot];
+      unsigned long long lo, hi;
+      ld_relaxed_b128(rec, lo, hi);
+      if (hi != tag) {
+        const unsigned long long t0 = globaltimer_ns();
+        unsigned n = 0;
+        do {
+          ld_relaxed_b128(rec, lo, hi);
+          if (hi != tag && (++n & 255u) == 0 && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
+            atomicOr(&ctl->status, kStatusExchangeTimeout);
+            break;
+          }
+        } while (hi != tag);
+      }
+      v = __longlong_as_double(static_cast<long long>(lo));
+    }
+    const unsigned n = min(32u, G - g0);
+    for (unsigned k = 0; k < n; ++k) tot += __shfl_sync(0xffffffffu, v, k);
+  }
+  return tot;
+}
+
 // ------------------------------------------------------ per-row sweep bodies --
 // A thread owns float4 chunks q = tid + k*NT (k < V) of the slice. FULL: every
 // chunk exists (slice == 4*NT*V); otherwise missing chunks carry 1.0f through
@@ -464,36 +501,8 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         for (int w = 1; w < NW; ++w) t += red[(q * NW + w) * BM + lane];
       }
       if (XCHG) {
-        // Publish {partial, tag} for the group, then gather all G partials of
-        // the row (one lane per CTA, spinning on L2: any back-off costs more
-        // than the polls) and sum them in ascending g: identical bits on every
-        // CTA of the group.
         TR_BEGIN();
-        if (lane == 0)
-          st_relaxed_b128(&a.xrec[static_cast<size_t>(cta) * kRing + (s % kRing)],
-                          static_cast<unsigned long long>(__double_as_longlong(t)), tag_hi | (s + 1));
-        double v = 0.0;
-        if (lane < static_cast<int>(G)) {
-          const ulonglong2* rec = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (s % kRing)];
-          const unsigned long long want = tag_hi | (s + 1);
-          unsigned long long lo, hi;
-          ld_relaxed_b128(rec, lo, hi);
-          if (hi != want) {
-            const unsigned long long t0 = globaltimer_ns();
-            unsigned n = 0;
-            do {
-              ld_relaxed_b128(rec, lo, hi);
-              if (hi != want && (++n & 255u) == 0 && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
-                atomicOr(&ctl->status, kStatusExchangeTimeout);
-                break;
-              }
-            } while (hi != want);
-          }
-          v = __longlong_as_double(static_cast<long long>(lo));
-        }
-        double tot = 0.0;
-        for (unsigned k = 0; k < G; ++k) tot += __shfl_sync(0xffffffffu, v, k);
-        t = tot;
+        t = exchange_row_sum(a.xrec, cta, group, G, s % kRing, tag_hi | (s + 1), t, ctl);
         TR_END(2);
       }
       TR_BEGIN();

@@ -311,33 +311,8 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_tmem_kernel(const
 #pragma unroll
         for (int w = 1; w < NW; ++w) t += red[(q * NW + w) * BM + lane];
       }
-      if (XCHG) {
-        // publish {partial, tag}; gather the G partials of the row, sum in ascending g
-        if (lane == 0)
-          st_relaxed_b128(&a.xrec[static_cast<size_t>(cta) * kRing + (s % kRing)],
-                          static_cast<unsigned long long>(__double_as_longlong(t)), tag_hi | (s + 1));
-        double v = 0.0;
-        if (lane < static_cast<int>(G)) {
-          const ulonglong2* rec = &a.xrec[static_cast<size_t>(group * G + lane) * kRing + (s % kRing)];
-          const unsigned long long want = tag_hi | (s + 1);
-          unsigned long long lo, hi;
-          ld_relaxed_b128(rec, lo, hi);
-          if (hi != want) {
-            const unsigned long long t0 = globaltimer_ns();
-            do {
-              ld_relaxed_b128(rec, lo, hi);
-              if (hi != want && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
-                atomicOr(&ctl->status, kStatusExchangeTimeout);
-                break;
-              }
-            } while (hi != want);
-          }
-          v = __longlong_as_double(static_cast<long long>(lo));
-        }
-        double tot = 0.0;
-        for (unsigned k = 0; k < G; ++k) tot += __shfl_sync(0xffffffffu, v, k);
-        t = tot;
-      }
+      if (XCHG) t = exchange_row_sum(a.xrec, cta, group, G, s % kRing, tag_hi | (s + 1), t, ctl);
+
       if (lane < static_cast<int>(nr)) {
         double al;
         if (!rescale_factor_dev(rv, t, a.fi, &al)) {

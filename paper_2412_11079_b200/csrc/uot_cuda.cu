@@ -319,9 +319,9 @@ int plan_layout(uot_ctx* ctx) {
   if (cols > (1ull << 26)) return ctx->fail(UOT_CONFIG_ERROR, "cols %llu too large", (unsigned long long)cols);
   const unsigned xmax = static_cast<unsigned>(env_int("UOT_SLICE_MAX_XCHG", kSliceMaxXchg));
   unsigned G = cols <= kSliceMax ? 1u : static_cast<unsigned>((cols + xmax - 1) / xmax);
-  if (G > static_cast<unsigned>(ctx->sms) || G > 32)
+  if (G > static_cast<unsigned>(ctx->sms))
     return ctx->fail(UOT_CONFIG_ERROR, "cols %llu needs %u CTAs per row (max %d)",
-                     (unsigned long long)cols, G, std::min(ctx->sms, 32));
+                     (unsigned long long)cols, G, ctx->sms);
   const unsigned slice = round_up(static_cast<unsigned>((cols + G - 1) / G), 4);
   const SweepCfg* cfg = nullptr;
   for (const auto& c : cfg_table())

@@ -293,3 +293,15 @@ def test_full_size_properties(gpu):
         s.init_col_sums()
         s.iterate(3, KNEVER)
         assert np.array_equal(plan[rows], s.plan()[rows])
+
+
+@pytest.mark.parametrize("m,n,k", [(40, 300000, 4), (9, 600000, 3)])
+def test_very_wide_rows(gpu, orc, m, n, k):
+    # G = ceil(cols / 8192) > 32 CTAs share a row: the exchange gathers the
+    # group's records 32 lanes at a time (no column limit below #SMs x 8192)
+    a, rpd, cpd = orc.gen_problem(17, m, n)
+    plan, f, cs, it, err, conv, lay = solve(gpu, a, rpd, cpd, 1.0, 0.1, k)
+    assert lay["G"] > 32 and it == k
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 4)
+    assert_parity(plan, ref.plan, rpd, cpd, f"{m}x{n}")
+    np.testing.assert_allclose(f.alpha, ref.alpha, rtol=1e-12)
