@@ -29,6 +29,7 @@
 #include <functional>
 #include <span>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -55,8 +56,8 @@ namespace uot::cuda {
 // A problem resident on one B200 (or one rank's row block of it).
 class Session {
  public:
-  Session(std::size_t rows, std::size_t cols, int device = 0) {
-    check(uot_create(&ctx_, rows, cols, UOT_F32, device));
+  Session(std::size_t rows, std::size_t cols, int device = 0, Dtype dtype = Dtype::f32) {
+    check(uot_create(&ctx_, rows, cols, dtype == Dtype::f64 ? UOT_F64 : UOT_F32, device));
   }
   // Rank `rank` of `nranks`, rows split by RankPartition::make (plan.cpp:35-44).
   Session(std::size_t global_rows, std::size_t cols, int device, int rank, int nranks,
@@ -97,6 +98,17 @@ class Session {
   void set_problem(const Problem<float>& p) {
     check(uot_set_problem(ctx_, p.a.data().data(), p.rpd.data(), p.cpd.data(), p.er, p.ep));
   }
+  // Problem<double> (Dtype::f64 session): plain f64 products, as fused.hpp:128-140 with T = double.
+  void set_problem(const Problem<double>& p) {
+    check(uot_set_problem_f64(ctx_, p.a.data().data(), p.rpd.data(), p.cpd.data(), p.er, p.ep));
+  }
+  void set_plan(const Matrix<double>& a) { check(uot_set_plan_f64(ctx_, a.data().data())); }
+  Matrix<double> plan_f64() const {
+    Matrix<double> m(rows(), cols());
+    check(uot_get_plan_f64(ctx_, m.data().data()));
+    return m;
+  }
+  Dtype dtype() const { return layout().dtype == UOT_F64 ? Dtype::f64 : Dtype::f32; }
   void set_fi(double fi) { check(uot_set_fi(ctx_, fi)); }
   // read_problem / write_problem (problem_io.cpp:97-141) of this session's rows,
   // streamed between the .uotp file and HBM.
@@ -156,21 +168,25 @@ class Session {
   uot_ctx* ctx_ = nullptr;
 };
 
-// fused_solve (fused.hpp:259-285) on one B200. The plan, factors and report
-// have the reference's meaning; report.solver is "cuda" and wall_ms also
-// covers the PCIe transfers.
-inline SolveResult<float> fused_solve(const Problem<float>& p, double tol, std::size_t max_iter,
-                                      int device = 0) {
+// fused_solve (fused.hpp:259-285) on one B200, for Problem<float> or
+// Problem<double>. The plan, factors and report have the reference's meaning;
+// report.solver is "cuda" and wall_ms also covers the PCIe transfers.
+template <typename T>
+inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t max_iter, int device = 0) {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "Problem<float> or Problem<double>");
   require_valid(p);
   if (!(tol > 0.0)) throw InvalidParameter("fused_solve: tol must be positive");
   if (max_iter < 1) throw InvalidParameter("fused_solve: max_iter must be at least 1");
   const auto t0 = std::chrono::steady_clock::now();
-  Session s(p.m(), p.n(), device);
+  Session s(p.m(), p.n(), device, std::is_same_v<T, double> ? Dtype::f64 : Dtype::f32);
   s.set_problem(p);
   s.init_col_sums();
   const auto pr = s.iterate(max_iter, tol);
-  SolveResult<float> r;
-  r.plan = s.plan();
+  SolveResult<T> r;
+  if constexpr (std::is_same_v<T, double>)
+    r.plan = s.plan_f64();
+  else
+    r.plan = s.plan();
   r.factors = s.factors();
   r.report.solver = "cuda";
   r.report.iterations = pr.iterations;
@@ -226,7 +242,7 @@ inline Session load(const std::filesystem::path& path, int device = 0) {
   double er = 0, ep = 0;
   const int rc = uot_problem_file_info(path.c_str(), &m, &n, &dtype, &er, &ep);
   if (rc != UOT_OK) raise(rc, uot_last_io_error());
-  Session s(m, n, device);
+  Session s(m, n, device, dtype == UOT_F64 ? Dtype::f64 : Dtype::f32);
   s.load_problem_file(path);
   return s;
 }

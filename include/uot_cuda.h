@@ -36,7 +36,10 @@ extern "C" {
 #define UOT_NCCL_ERROR 6        /* NCCL failure (no reference analogue) */
 #define UOT_IO_ERROR 7          /* uot::IoError (problem file container) */
 
-/* Dtype codes: uot::Dtype (include/uot/matrix.hpp:13). Only f32 has a kernel. */
+/* Dtype codes: uot::Dtype (include/uot/matrix.hpp:13). Both have a kernel: f32
+ * storage with f64 arithmetic (the products rounded once to fp32, as T(double)
+ * in fused.hpp:128-140), or f64 storage (plain f64 products). The resident,
+ * TMEM, persistent and ablation paths are f32-only. */
 #define UOT_F32 1
 #define UOT_F64 2
 
@@ -70,6 +73,7 @@ typedef struct uot_layout {
   int32_t tmem;          /* iterations park the alpha-lag rows in Tensor Memory (sweep_tmem.cuh) */
   int32_t resident;      /* uot_iterate runs as ONE persistent launch, matrix in shared memory (resident.cuh) */
   int32_t persist;       /* otherwise, single rank: ONE persistent streaming launch (persist.cuh) */
+  int32_t dtype;         /* UOT_F32 (Problem<float>) or UOT_F64 (Problem<double>) */
 } uot_layout;
 
 /* ---- sessions ---------------------------------------------------------- */
@@ -144,7 +148,10 @@ UOT_API void* uot_get_stream(const uot_ctx* ctx);
  * compute_fi(er, ep) (scaling.cpp:9-13). Resets the iteration state. */
 UOT_API int uot_set_problem(uot_ctx* ctx, const float* a, const double* rpd, const double* cpd, double er,
                     double ep);
-/* gen_problem_t<float>(seed, global_rows, cols) (problem_io.hpp:17-31) generated
+/* Problem<double> (Dtype::f64 sessions): same contract, fp64 matrix. */
+UOT_API int uot_set_problem_f64(uot_ctx* ctx, const double* a, const double* rpd, const double* cpd, double er,
+                                double ep);
+/* gen_problem_t<T>(seed, global_rows, cols) (problem_io.hpp:17-31) generated
  * directly in HBM, bit-identical to the host generator, then er/ep applied. */
 UOT_API int uot_generate_problem(uot_ctx* ctx, uint64_t seed, double er, double ep);
 /* Override the damping exponent (fused_iterate takes fi directly, fused.hpp:165).
@@ -152,6 +159,7 @@ UOT_API int uot_generate_problem(uot_ctx* ctx, uint64_t seed, double er, double 
 UOT_API int uot_set_fi(uot_ctx* ctx, double fi);
 /* Replace only the plan (the current matrix) of this rank; marginals stay. */
 UOT_API int uot_set_plan(uot_ctx* ctx, const float* a);
+UOT_API int uot_set_plan_f64(uot_ctx* ctx, const double* a);
 
 /* ---- the path ---------------------------------------------------------- */
 
@@ -186,6 +194,7 @@ UOT_API int uot_synchronize(uot_ctx* ctx);
 UOT_API int uot_get_factors(const uot_ctx* ctx, double* alpha, double* beta);
 /* The plan (rows x cols row-major) of this rank. */
 UOT_API int uot_get_plan(const uot_ctx* ctx, float* out);
+UOT_API int uot_get_plan_f64(const uot_ctx* ctx, double* out);
 /* Completed iterations and the error of the last one. */
 UOT_API int uot_get_report(const uot_ctx* ctx, uint64_t* iterations, double* final_error, int* converged);
 /* CommStats (distributed.hpp:24-27). */
@@ -212,6 +221,8 @@ UOT_API int uot_rank_partition(uint64_t ranks, uint64_t rows, uint64_t* bounds);
  * block's A, its rpd slice and the full cpd (either may be NULL). */
 UOT_API int uot_gen_block_f32(uint64_t seed, uint64_t global_rows, uint64_t n, uint64_t row0,
                               uint64_t rows, float* a, double* rpd, double* cpd, int threads);
+UOT_API int uot_gen_block_f64(uint64_t seed, uint64_t global_rows, uint64_t n, uint64_t row0,
+                              uint64_t rows, double* a, double* rpd, double* cpd, int threads);
 /* gen_problem_t<float> on the host (threads > 1 fills A in parallel). */
 UOT_API int uot_gen_problem_f32(uint64_t seed, uint64_t m, uint64_t n, float* a, double* rpd, double* cpd,
                         int threads);

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) persist_kernel(const Pe
   const unsigned nb = (nrows + B - 1) / B;
   const unsigned nq = a.slice >> 2;
   const uint32_t row_bytes = a.slice * 4u;
-  float* gbase = a.P + r0 * a.pitch + static_cast<size_t>(g) * a.slice;
+  float* gbase = static_cast<float*>(a.P) + r0 * a.pitch + static_cast<size_t>(g) * a.slice;
   const unsigned K = pa.k;
 
   if (tid == 0) {

@@ -21,15 +21,17 @@ __device__ __forceinline__ double splitmix_unit_at(uint64_t seed, uint64_t k) {
 }
 
 // A (local rows [row0, row0+rows) of a global rows x cols problem) into the
-// pitched layout; padding columns are zero.
-__global__ void gen_matrix_kernel(float* P, uint64_t seed, unsigned long long row0,
+// pitched layout; padding columns are zero. T = float: the draw cast to fp32
+// (gen_problem_t<float>), T = double: the draw itself.
+template <typename T>
+__global__ void gen_matrix_kernel(T* P, uint64_t seed, unsigned long long row0,
                                   unsigned long long rows, unsigned cols, unsigned pitch) {
   const unsigned long long n = rows * pitch;
   for (unsigned long long idx = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
        idx < n; idx += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
     const unsigned long long i = idx / pitch;
     const unsigned j = static_cast<unsigned>(idx - i * pitch);
-    P[idx] = j < cols ? static_cast<float>(splitmix_unit_at(seed, (row0 + i) * cols + j)) : 0.0f;
+    P[idx] = j < cols ? static_cast<T>(splitmix_unit_at(seed, (row0 + i) * cols + j)) : T(0);
   }
 }
 
@@ -49,27 +51,29 @@ __global__ void gen_marginals_kernel(double* rpd, double* cpd, uint64_t seed,
 
 // validate_problem's matrix rule (include/uot/problem.hpp:85-90): every entry
 // strictly positive and finite. Padding columns are skipped. Sets *bad.
-__global__ void validate_matrix_kernel(const float* P, unsigned long long rows, unsigned cols,
+template <typename T>
+__global__ void validate_matrix_kernel(const T* P, unsigned long long rows, unsigned cols,
                                        unsigned pitch, int* bad) {
   const unsigned long long n = rows * pitch;
   int local = 0;
   for (unsigned long long idx = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
        idx < n; idx += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
     const unsigned j = static_cast<unsigned>(idx % pitch);
-    const float v = P[idx];
-    if (j < cols && !(v > 0.0f && isfinite(v))) local = 1;
+    const T v = P[idx];
+    if (j < cols && !(v > T(0) && isfinite(v))) local = 1;
   }
   if (__syncthreads_or(local) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
 // Zero the padding columns [cols, pitch) after a host upload.
-__global__ void zero_padding_kernel(float* P, unsigned long long rows, unsigned cols, unsigned pitch) {
+template <typename T>
+__global__ void zero_padding_kernel(T* P, unsigned long long rows, unsigned cols, unsigned pitch) {
   const unsigned w = pitch - cols;
   const unsigned long long n = rows * w;
   for (unsigned long long idx = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
        idx < n; idx += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
     const unsigned long long i = idx / w;
-    P[i * pitch + cols + (idx - i * w)] = 0.0f;
+    P[i * pitch + cols + (idx - i * w)] = T(0);
   }
 }
 

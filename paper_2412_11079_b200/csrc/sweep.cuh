@@ -36,6 +36,7 @@
 //     (F2F.F32.F64), f64 sums of the stored fp32 values (see ScreenBounds).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "ptx.cuh"
 #include "uot_device.cuh"
@@ -43,7 +44,7 @@
 namespace uotk {
 
 struct SweepArgs {
-  float* P;                   // [rows][pitch] fp32, device layout
+  void* P;                    // [rows][pitch] fp32 (or fp64: Problem<double>), device layout
   const double* beta2;        // [2][pitch] column factors; beta(t) lives in slot t&1
   const double* rpd;          // [rows] row marginals
   double* alpha;              // [rows] row factors (output)
@@ -339,6 +340,71 @@ __device__ __forceinline__ void row_seed(const float4* row, unsigned tid, unsign
   }
 }
 
+// ---- Problem<double> (Dtype::f64) bodies: fused.hpp:128-140 with T = double,
+// so x1 = x0*beta_j and x2 = x1*alpha are plain f64 products (no rounding to a
+// narrower type) and the sums add them directly. A thread owns double2 chunks
+// q = tid + k*NT (k < V).
+template <int NT, int V, bool FULL>
+__device__ __forceinline__ double row_sweep1_f64(double2* row, unsigned tid, unsigned nq, const double* beta) {
+  double2 v[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    v[k] = (FULL || q < nq) ? row[q] : make_double2(0.0, 0.0);
+  }
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    v[k].x *= beta[2 * k];
+    v[k].y *= beta[2 * k + 1];
+    if (FULL || q < nq) {
+      row[q] = v[k];
+      s0 += v[k].x;
+      s1 += v[k].y;
+    }
+  }
+  return s0 + s1;
+}
+template <int NT, int V, bool FULL>
+__device__ __forceinline__ void row_sweep2_f64(double2* row, unsigned tid, unsigned nq, double al, double* acc) {
+  double2 v[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    v[k] = (FULL || q < nq) ? row[q] : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    v[k].x *= al;
+    v[k].y *= al;
+    if (FULL || q < nq) {
+      row[q] = v[k];
+      acc[2 * k] += v[k].x;
+      acc[2 * k + 1] += v[k].y;
+    }
+  }
+}
+template <int NT, int V, bool FULL>
+__device__ __forceinline__ void row_seed_f64(const double2* row, unsigned tid, unsigned nq, double* acc) {
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const unsigned q = tid + k * NT;
+    if (FULL || q < nq) {
+      const double2 v = row[q];
+      acc[2 * k] += v.x;
+      acc[2 * k + 1] += v.y;
+    }
+  }
+}
+
+// Elements per 16-byte chunk of the storage type.
+template <typename T>
+constexpr int elems_per_chunk() {
+  return static_cast<int>(16 / sizeof(T));
+}
+
 // Shared-memory layout shared by host sizing and the kernel.
 template <int NW, int BM, int NBUF>
 struct SweepSmem {
@@ -353,10 +419,13 @@ struct SweepSmem {
 // thread per row (slice <= 4*NT*V; FULL: equality), BM max rows per batch, NBUF
 // ring slots. LA: batches between sweep 1 and sweep 2 of a batch beyond the
 // next one (the factor warps' latency budget). XCHG: G > 1, row sums are
-// exchanged across the group. SEED: the read-only init_col_sums sweep.
-template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED>
+// exchanged across the group. SEED: the read-only init_col_sums sweep. T: the
+// storage type of P (float: Problem<float>, double: Problem<double>).
+template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED, typename T = float>
 __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const SweepArgs a) {
   constexpr int NW = NT / 32;
+  constexpr bool F64 = std::is_same<T, double>::value;
+  constexpr int EPC = elems_per_chunk<T>();  // 4 floats or 2 doubles per 16-byte chunk
   static_assert(NF >= 1 && NF <= kErrSlots, "factor warps");
   static_assert(LA >= 1 && LA <= 2 && (!XCHG || LA == 2), "lag (the alpha / red rings hold kQ batches)");
   static_assert(NBUF >= LA + 4, "ring too small");
@@ -392,9 +461,9 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   const unsigned nrows = static_cast<unsigned>(base + (group < rem ? 1 : 0));
   const unsigned B = a.B;
   const unsigned nb = (nrows + B - 1) / B;
-  const unsigned nq = a.slice >> 2;
-  const uint32_t row_bytes = a.slice * 4u;
-  float* gbase = a.P + r0 * a.pitch + static_cast<size_t>(g) * a.slice;
+  const unsigned nq = a.slice / EPC;
+  const uint32_t row_bytes = a.slice * static_cast<uint32_t>(sizeof(T));
+  T* gbase = static_cast<T*>(a.P) + r0 * a.pitch + static_cast<size_t>(g) * a.slice;
 
   if (tid == 0) {
     for (int i = 0; i < NBUF; ++i) {
@@ -409,8 +478,8 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   }
   __syncthreads();
 
-  auto slot_ptr = [&](unsigned b) -> float* {
-    return reinterpret_cast<float*>(smem + (b % NBUF) * a.buf_stride);
+  auto slot_ptr = [&](unsigned b) -> T* {
+    return reinterpret_cast<T*>(smem + (b % NBUF) * a.buf_stride);
   };
   auto rows_in = [&](unsigned b) -> unsigned { return min(B, nrows - b * B); };
   TR_DECL
@@ -424,8 +493,8 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     auto issue_load = [&](unsigned b) {
       const unsigned nr = rows_in(b);
       uint64_t* bar = &full[b % NBUF];
-      float* dst = slot_ptr(b);
-      const float* src = gbase + static_cast<size_t>(b) * B * a.pitch;
+      T* dst = slot_ptr(b);
+      const T* src = gbase + static_cast<size_t>(b) * B * a.pitch;
       mbar_arrive_expect_tx(bar, nr * row_bytes);
       if (G == 1) {
         bulk_g2s(dst, src, nr * row_bytes, bar, pol);  // rows contiguous when G == 1
@@ -436,8 +505,8 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     };
     auto issue_store = [&](unsigned b) {
       const unsigned nr = rows_in(b);
-      const float* srcs = slot_ptr(b);
-      float* dst = gbase + static_cast<size_t>(b) * B * a.pitch;
+      const T* srcs = slot_ptr(b);
+      T* dst = gbase + static_cast<size_t>(b) * B * a.pitch;
       if (G == 1) {
         bulk_s2g(dst, srcs, nr * row_bytes, pol);
       } else {
@@ -538,9 +607,9 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   }
 
   // ========================================================= compute warps ==
-  double beta[4 * V], acc[4 * V];
+  double beta[EPC * V], acc[EPC * V];
 #pragma unroll
-  for (int i = 0; i < 4 * V; ++i) acc[i] = 0.0;
+  for (int i = 0; i < EPC * V; ++i) acc[i] = 0.0;
   ScreenBounds sb{0xffffffffu, 0u};
   if (!SEED) {
     const double* bsrc = a.beta2 + ((ctl->iter + 1) & 1ull) * a.pitch + static_cast<size_t>(g) * a.slice;
@@ -548,9 +617,9 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     for (int k = 0; k < V; ++k) {
       const unsigned q = tid + k * NT;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) beta[4 * k + e] = (FULL || q < nq) ? bsrc[4 * q + e] : 1.0;
+      for (int e = 0; e < EPC; ++e) beta[EPC * k + e] = (FULL || q < nq) ? bsrc[EPC * q + e] : 1.0;
     }
-    sb = screen_bounds(beta, 4 * V);
+    if (!F64) sb = screen_bounds(beta, EPC * V);
   }
 
 #ifdef UOT_TRACE
@@ -559,12 +628,16 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   if (SEED) {
     for (unsigned s = 0; s < nb; ++s) {
       mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
-      const float* buf = slot_ptr(s);
+      const T* buf = slot_ptr(s);
       const unsigned nr = rows_in(s);
 #pragma unroll
       for (int r = 0; r < BM; ++r)
-        if (r < static_cast<int>(nr))
-          row_seed<NT, V, FULL>(reinterpret_cast<const float4*>(buf + r * a.slice), tid, nq, acc);
+        if (r < static_cast<int>(nr)) {
+          if constexpr (F64)
+            row_seed_f64<NT, V, FULL>(reinterpret_cast<const double2*>(buf + r * a.slice), tid, nq, acc);
+          else
+            row_seed<NT, V, FULL>(reinterpret_cast<const float4*>(buf + r * a.slice), tid, nq, acc);
+        }
       __syncwarp();
       if (lane == 0) mbar_arrive(&done2[s % NBUF]);
     }
@@ -579,7 +652,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         TR_BEGIN();
         mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
         TR_END(16);
-        float* buf = slot_ptr(s);
+        T* buf = slot_ptr(s);
         const unsigned nr = rows_in(s);
         const unsigned sh = (s % 8) * 8;
         x1bad &= ~(0xffull << sh);
@@ -587,9 +660,14 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         for (int r = 0; r < BM; ++r) {
           part[r] = 0.0;
           if (r < static_cast<int>(nr)) {
-            bool bad = false;
-            part[r] = row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, sb, bad);
-            if (bad) x1bad |= 1ull << (sh + r);
+            if constexpr (F64) {
+              part[r] = row_sweep1_f64<NT, V, FULL>(reinterpret_cast<double2*>(buf + r * a.slice), tid, nq, beta);
+            } else {
+              bool bad = false;
+              part[r] =
+                  row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, sb, bad);
+              if (bad) x1bad |= 1ull << (sh + r);
+            }
           }
         }
       }
@@ -597,14 +675,19 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         TR_BEGIN();
         mbar_wait(&alpha_rdy[b % kQ], (b / kQ) & 1u);
         TR_END(19);
-        float* buf = slot_ptr(b);
+        T* buf = slot_ptr(b);
         const unsigned nr = rows_in(b);
         const unsigned sh = (b % 8) * 8;
 #pragma unroll
         for (int r = 0; r < BM; ++r)
-          if (r < static_cast<int>(nr))
-            row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq,
-                                    alpha_s[(b % kQ) * BM + r], (x1bad >> (sh + r)) & 1ull, acc);
+          if (r < static_cast<int>(nr)) {
+            if constexpr (F64)
+              row_sweep2_f64<NT, V, FULL>(reinterpret_cast<double2*>(buf + r * a.slice), tid, nq,
+                                          alpha_s[(b % kQ) * BM + r], acc);
+            else
+              row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq,
+                                      alpha_s[(b % kQ) * BM + r], (x1bad >> (sh + r)) & 1ull, acc);
+          }
         fence_proxy_async_smem();  // generic writes -> the producer's bulk store
         __syncwarp();
         if (lane == 0) mbar_arrive(&done2[b % NBUF]);
@@ -637,8 +720,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   for (int k = 0; k < V; ++k) {
     const unsigned q = tid + k * NT;
     if (q < nq) {
-      reinterpret_cast<double2*>(dst)[2 * q] = make_double2(acc[4 * k + 0], acc[4 * k + 1]);
-      reinterpret_cast<double2*>(dst)[2 * q + 1] = make_double2(acc[4 * k + 2], acc[4 * k + 3]);
+#pragma unroll
+      for (int h = 0; h < EPC / 2; ++h)
+        reinterpret_cast<double2*>(dst)[(EPC / 2) * q + h] =
+            make_double2(acc[EPC * k + 2 * h], acc[EPC * k + 2 * h + 1]);
     }
   }
 }

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_tmem_kernel(const
   const unsigned nb = (nrows + B - 1) / B;
   const unsigned nq = a.slice >> 2;
   const uint32_t row_bytes = a.slice * 4u;
-  float* gbase = a.P + r0 * a.pitch + static_cast<size_t>(g) * a.slice;
+  float* gbase = static_cast<float*>(a.P) + r0 * a.pitch + static_cast<size_t>(g) * a.slice;
   auto rows_in = [&](unsigned b) -> unsigned { return min(B, nrows - b * B); };
   auto lslot = [&](unsigned b) -> float* { return reinterpret_cast<float*>(lring + (b % NL) * a.buf_stride); };
   auto sslot = [&](unsigned b) -> float* { return reinterpret_cast<float*>(sring + (b % NS) * a.buf_stride); };

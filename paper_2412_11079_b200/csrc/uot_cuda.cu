@@ -132,6 +132,35 @@ const std::vector<ResidentCfg>& rcfg_table() {
   return t;
 }
 
+// Problem<double>: the same kernel over fp64 storage (double2 chunks, 32 KiB =
+// 4096-double slices); the ring/TMEM/persistent variants are fp32-only.
+template <int NT, int V, int BM, int NB, bool XCHG = false>
+SweepCfg make_cfg_f64() {
+  constexpr int LA = XCHG ? UOT_LA_X : UOT_LA_G1;
+  constexpr int NF = XCHG ? UOT_NF_X : UOT_NF_G1;
+  SweepCfg c{};
+  c.nt = NT;
+  c.v = V;
+  c.bm = BM;
+  c.nbuf = NB;
+  c.nf = NF;
+  c.xchg = XCHG;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false, double>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false, double>;
+  c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true, double>;
+  c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true, double>;
+  c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
+  return c;
+}
+const std::vector<SweepCfg>& cfg_table_f64() {
+  static const std::vector<SweepCfg> t = {
+      make_cfg_f64<128, 1, 4, 7>(), make_cfg_f64<256, 1, 8, 7>(), make_cfg_f64<512, 1, 4, 7>(),
+      make_cfg_f64<512, 2, 2, 7>(), make_cfg_f64<512, 4, 1, 7>(),
+      make_cfg_f64<512, 3, 1, 7, true>(), make_cfg_f64<512, 4, 1, 7, true>(),
+  };
+  return t;
+}
+
 const std::vector<SweepCfg>& cfg_table() {
   static const std::vector<SweepCfg> t = {
       // G == 1 (rows fit one CTA): 32 KiB ring slots
@@ -239,7 +268,10 @@ struct uot_ctx {
   bool use_persist = false;  // uot_iterate is one persistent streaming launch (persist.cuh, opt-in)
 
   // device buffers
-  float* P = nullptr;
+  void* P = nullptr;          // [rows][pitch] of `dtype` (float or double)
+  int dtype = UOT_F32;
+  unsigned esz = 4;           // bytes per element
+  float* Pf() const { return static_cast<float*>(P); }
   double *rpd = nullptr, *cpd = nullptr, *alpha = nullptr, *beta2 = nullptr, *col_sums = nullptr,
          *xsum = nullptr, *partials = nullptr, *cta_err = nullptr;
   ulonglong2* xrec = nullptr;
@@ -317,35 +349,38 @@ int probe_smid_map(uot_ctx* ctx) {
 int plan_layout(uot_ctx* ctx) {
   const uint64_t cols = ctx->cols;
   if (cols > (1ull << 26)) return ctx->fail(UOT_CONFIG_ERROR, "cols %llu too large", (unsigned long long)cols);
-  const unsigned xmax = static_cast<unsigned>(env_int("UOT_SLICE_MAX_XCHG", kSliceMaxXchg));
-  unsigned G = cols <= kSliceMax ? 1u : static_cast<unsigned>((cols + xmax - 1) / xmax);
+  const bool f64 = ctx->dtype == UOT_F64;
+  const unsigned epc = 16 / ctx->esz;  // elements per 16-byte chunk
+  const unsigned smax = kSliceMax * 4 / ctx->esz;  // 32 KiB of elements
+  const unsigned xmax = static_cast<unsigned>(env_int("UOT_SLICE_MAX_XCHG", kSliceMaxXchg)) * 4 / ctx->esz;
+  unsigned G = cols <= smax ? 1u : static_cast<unsigned>((cols + xmax - 1) / xmax);
   if (G > static_cast<unsigned>(ctx->sms))
     return ctx->fail(UOT_CONFIG_ERROR, "cols %llu needs %u CTAs per row (max %d)",
                      (unsigned long long)cols, G, ctx->sms);
-  const unsigned slice = round_up(static_cast<unsigned>((cols + G - 1) / G), 4);
+  const unsigned slice = round_up(static_cast<unsigned>((cols + G - 1) / G), epc);
   const SweepCfg* cfg = nullptr;
-  for (const auto& c : cfg_table())
-    if (static_cast<unsigned>(c.nt * 4 * c.v) >= slice && c.xchg == (G > 1)) {
+  for (const auto& c : f64 ? cfg_table_f64() : cfg_table())
+    if (static_cast<unsigned>(c.nt) * epc * c.v >= slice && c.xchg == (G > 1)) {
       cfg = &c;
       break;
     }
-  if (!cfg) return ctx->fail(UOT_CONFIG_ERROR, "no sweep configuration covers a %u-float slice", slice);
+  if (!cfg) return ctx->fail(UOT_CONFIG_ERROR, "no sweep configuration covers a %u-element slice", slice);
   ctx->G = G;
   ctx->slice = slice;
   ctx->pitch = slice * G;
   ctx->cfg = cfg;
-  ctx->B = G > 1 ? 1u : std::max(1u, std::min(static_cast<unsigned>(cfg->bm), kSliceMax / slice));
+  ctx->B = G > 1 ? 1u : std::max(1u, std::min(static_cast<unsigned>(cfg->bm), smax / slice));
   ctx->groups = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->rows, ctx->sms / G)));
   ctx->grid = ctx->groups * G;
-  ctx->buf_stride = round_up(ctx->B * slice * 4u, 128);
+  ctx->buf_stride = round_up(ctx->B * slice * ctx->esz, 128);
   ctx->smem = cfg->smem_bytes(ctx->buf_stride);
-  ctx->smem_tm = cfg->smem_bytes_tm(ctx->buf_stride);
+  ctx->smem_tm = f64 ? 0 : cfg->smem_bytes_tm(ctx->buf_stride);
   int smem_optin = 0;
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   // the TMEM-lag kernel's rings + factor rings must fit next to each other
-  ctx->use_tmem = env_int("UOT_TMEM", 0) != 0 && ctx->smem_tm <= static_cast<size_t>(smem_optin);
-  ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * 4 > (64ull << 20) ? 1 : 0;
-  ctx->full = slice == static_cast<unsigned>(4 * cfg->nt * cfg->v) ? 1 : 0;
+  ctx->use_tmem = !f64 && env_int("UOT_TMEM", 0) != 0 && ctx->smem_tm <= static_cast<size_t>(smem_optin);
+  ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * ctx->esz > (64ull << 20) ? 1 : 0;
+  ctx->full = slice == epc * cfg->nt * cfg->v ? 1 : 0;
   int rc = probe_smid_map(ctx);
   if (rc) return rc;
   for (SweepFn fn : {cfg->iter[ctx->full], cfg->seed[ctx->full]}) {
@@ -365,7 +400,7 @@ int plan_layout(uot_ctx* ctx) {
   // Every CTA must stream more than NBUF batches per iteration: the producer then
   // never prefetches a row batch before its previous-iteration store was issued.
   const uint64_t nb_min = (ctx->rows / ctx->groups) / ctx->B;
-  ctx->use_persist = ctx->nranks == 1 && !ctx->use_tmem && env_int("UOT_PERSIST", 0) != 0 &&
+  ctx->use_persist = !f64 && ctx->nranks == 1 && !ctx->use_tmem && env_int("UOT_PERSIST", 0) != 0 &&
                      ctx->groups <= 160 && nb_min > static_cast<uint64_t>(cfg->nbuf);
   if (ctx->use_persist)
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(cfg->persist[ctx->full]),
@@ -373,7 +408,7 @@ int plan_layout(uot_ctx* ctx) {
   // Resident mode (resident.cuh): one rank, rows fit one CTA (G == 1), a CTA's
   // row block fits shared memory and at most 32 rows per CTA. UOT_RESIDENT=0: off.
   ctx->rcfg = nullptr;
-  if (ctx->nranks == 1 && G == 1 && env_int("UOT_RESIDENT", 1)) {
+  if (!f64 && ctx->nranks == 1 && G == 1 && env_int("UOT_RESIDENT", 1)) {
     const unsigned rgrid = static_cast<unsigned>(std::min<uint64_t>(ctx->rows, ctx->sms));
     const uint64_t rows_cta = (ctx->rows + rgrid - 1) / rgrid;
     const unsigned nq = ctx->pitch / 4;
@@ -403,7 +438,7 @@ int dalloc(uot_ctx* ctx, T** p, size_t count) {
 int alloc_all(uot_ctx* ctx) {
   const size_t rows = ctx->rows, pitch = ctx->pitch;
   int rc;
-  if ((rc = dalloc(ctx, &ctx->P, rows * pitch))) return rc;
+  if ((rc = ctx->cuda(cudaMalloc(&ctx->P, std::max<size_t>(rows * pitch, 1) * ctx->esz), "cudaMalloc"))) return rc;
   if ((rc = dalloc(ctx, &ctx->rpd, rows))) return rc;
   if ((rc = dalloc(ctx, &ctx->alpha, rows))) return rc;
   if ((rc = dalloc(ctx, &ctx->cpd, pitch))) return rc;
@@ -509,7 +544,7 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
 // ------------------------------------------------------------ ablations --
 AblArgs abl_args(const uot_ctx* ctx) {
   AblArgs a;
-  a.P = ctx->P;
+  a.P = ctx->Pf();
   a.beta2 = ctx->beta2;
   a.rpd = ctx->rpd;
   a.alpha = ctx->alpha;
@@ -585,7 +620,7 @@ int launch_persist(uot_ctx* ctx, uint64_t k) {
 // The whole iterate(k) call as one cooperative launch (resident.cuh).
 int launch_resident(uot_ctx* ctx, uint64_t k) {
   ResidentArgs r;
-  r.P = ctx->P;
+  r.P = ctx->Pf();
   r.beta2 = ctx->beta2;
   r.rpd = ctx->rpd;
   r.cpd = ctx->cpd;
@@ -693,11 +728,21 @@ int check_marginals(uot_ctx* ctx, const double* rpd, const double* cpd, double e
 int after_matrix_upload(uot_ctx* ctx) {
   const unsigned gblocks = static_cast<unsigned>(ctx->sms) * 8;
   if (ctx->pitch > ctx->cols) {
-    zero_padding_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->P, ctx->rows, static_cast<unsigned>(ctx->cols), ctx->pitch);
+    if (ctx->dtype == UOT_F64)
+      zero_padding_kernel<<<gblocks, 256, 0, ctx->stream>>>(static_cast<double*>(ctx->P), ctx->rows,
+                                                             static_cast<unsigned>(ctx->cols), ctx->pitch);
+    else
+      zero_padding_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->Pf(), ctx->rows, static_cast<unsigned>(ctx->cols),
+                                                             ctx->pitch);
     ctx->launches++;
   }
   CK(cudaMemsetAsync(ctx->dflag, 0, sizeof(int), ctx->stream));
-  validate_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->P, ctx->rows, static_cast<unsigned>(ctx->cols), ctx->pitch, ctx->dflag);
+  if (ctx->dtype == UOT_F64)
+    validate_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(static_cast<const double*>(ctx->P), ctx->rows,
+                                                              static_cast<unsigned>(ctx->cols), ctx->pitch, ctx->dflag);
+  else
+    validate_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->Pf(), ctx->rows, static_cast<unsigned>(ctx->cols),
+                                                              ctx->pitch, ctx->dflag);
   ctx->launches++;
   CK(cudaGetLastError());
   int bad = 0;
@@ -735,8 +780,10 @@ int uot_create(uot_ctx** out, uint64_t rows, uint64_t cols, int dtype, int devic
   auto* ctx = new uot_ctx();
   *out = ctx;
   if (rows < 1 || cols < 1) return ctx->fail(UOT_INVALID_PARAMETER, "matrix must be at least 1x1");
-  if (dtype != UOT_F32)
-    return ctx->fail(UOT_INVALID_PARAMETER, "dtype %d: only f32 (Dtype::f32) has an sm_100a kernel", dtype);
+  if (dtype != UOT_F32 && dtype != UOT_F64)
+    return ctx->fail(UOT_INVALID_PARAMETER, "dtype %d: neither f32 nor f64 (Dtype, matrix.hpp:13)", dtype);
+  ctx->dtype = dtype;
+  ctx->esz = dtype == UOT_F64 ? 8 : 4;
   ctx->rows = ctx->global_rows = rows;
   ctx->cols = cols;
   return create_common(ctx, device);
@@ -762,8 +809,10 @@ int create_rank(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, i
   auto* ctx = new uot_ctx();
   *out = ctx;
   if (global_rows < 1 || cols < 1) return ctx->fail(UOT_INVALID_PARAMETER, "matrix must be at least 1x1");
-  if (dtype != UOT_F32)
-    return ctx->fail(UOT_INVALID_PARAMETER, "dtype %d: only f32 (Dtype::f32) has an sm_100a kernel", dtype);
+  if (dtype != UOT_F32 && dtype != UOT_F64)
+    return ctx->fail(UOT_INVALID_PARAMETER, "dtype %d: neither f32 nor f64 (Dtype, matrix.hpp:13)", dtype);
+  ctx->dtype = dtype;
+  ctx->esz = dtype == UOT_F64 ? 8 : 4;
   if (nranks < 1 || static_cast<uint64_t>(nranks) > global_rows)  // plan.cpp:36-39
     return ctx->fail(UOT_PARTITION_ERROR, "RankPartition: %d ranks for %llu rows would leave a rank without rows",
                      nranks, (unsigned long long)global_rows);
@@ -862,6 +911,8 @@ int uot_set_variant(uot_ctx* ctx, int variant) {
     return ctx->fail(UOT_INVALID_PARAMETER, "unknown iteration variant %d", variant);
   if (variant != UOT_VARIANT_FUSED && ctx->nranks > 1)
     return ctx->fail(UOT_INVALID_PARAMETER, "the ablation schedules are single-GPU only");
+  if (variant != UOT_VARIANT_FUSED && ctx->dtype != UOT_F32)
+    return ctx->fail(UOT_INVALID_PARAMETER, "the ablation schedules are fp32 only");
   CK(cudaSetDevice(ctx->device));
   if (variant != UOT_VARIANT_FUSED && !ctx->abl_partials) {
     ctx->abl_gx = (ctx->pitch / 4 + kAblColThreads * kAblColV - 1) / (kAblColThreads * kAblColV);
@@ -919,6 +970,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->tmem = ctx->use_tmem ? 1 : 0;
   o->resident = ctx->rcfg ? 1 : 0;
   o->persist = ctx->use_persist ? 1 : 0;
+  o->dtype = ctx->dtype;
   o->nbuf = ctx->cfg->nbuf;
   o->sms = ctx->sms;
   o->rank = ctx->rank;
@@ -932,23 +984,63 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
 
 void* uot_get_stream(const uot_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 
-int uot_set_problem(uot_ctx* ctx, const float* a, const double* rpd, const double* cpd, double er,
-                    double ep) {
-  if (!ctx || !a || !rpd || !cpd) return UOT_INVALID_PARAMETER;
+}  // extern "C"
+
+namespace {
+int dtype_check(uot_ctx* ctx, int want, const char* who) {
+  if (ctx->dtype == want) return UOT_OK;
+  return ctx->fail(UOT_INVALID_PARAMETER, "%s: the session holds a Problem<%s>", who,
+                   ctx->dtype == UOT_F64 ? "double" : "float");
+}
+
+int set_problem_any(uot_ctx* ctx, const void* a, const double* rpd, const double* cpd, double er, double ep) {
   CK(cudaSetDevice(ctx->device));
   int rc = check_marginals(ctx, rpd, cpd, er, ep);
   if (rc) return rc;
   ctx->er = er;
   ctx->ep = ep;
   ctx->have_problem = false;
-  CK(cudaMemcpy2DAsync(ctx->P, ctx->pitch * sizeof(float), a, ctx->cols * sizeof(float),
-                       ctx->cols * sizeof(float), ctx->rows, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpy2DAsync(ctx->P, ctx->pitch * ctx->esz, a, ctx->cols * ctx->esz, ctx->cols * ctx->esz, ctx->rows,
+                       cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->rpd, rpd, ctx->rows * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->cpd, cpd, ctx->cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   if ((rc = reset_state(ctx))) return rc;
   if ((rc = after_matrix_upload(ctx))) return rc;
   ctx->have_problem = true;
   return UOT_OK;
+}
+
+int set_plan_any(uot_ctx* ctx, const void* a) {
+  if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpy2DAsync(ctx->P, ctx->pitch * ctx->esz, a, ctx->cols * ctx->esz, ctx->cols * ctx->esz, ctx->rows,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  return after_matrix_upload(ctx);
+}
+
+int get_plan_any(uot_ctx* ctx, void* out) {
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpy2DAsync(out, ctx->cols * ctx->esz, ctx->P, ctx->pitch * ctx->esz, ctx->cols * ctx->esz, ctx->rows,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return UOT_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int uot_set_problem(uot_ctx* ctx, const float* a, const double* rpd, const double* cpd, double er,
+                    double ep) {
+  if (!ctx || !a || !rpd || !cpd) return UOT_INVALID_PARAMETER;
+  int rc = dtype_check(ctx, UOT_F32, "uot_set_problem");
+  return rc ? rc : set_problem_any(ctx, a, rpd, cpd, er, ep);
+}
+
+int uot_set_problem_f64(uot_ctx* ctx, const double* a, const double* rpd, const double* cpd, double er,
+                        double ep) {
+  if (!ctx || !a || !rpd || !cpd) return UOT_INVALID_PARAMETER;
+  int rc = dtype_check(ctx, UOT_F64, "uot_set_problem_f64");
+  return rc ? rc : set_problem_any(ctx, a, rpd, cpd, er, ep);
 }
 
 int uot_generate_problem(uot_ctx* ctx, uint64_t seed, double er, double ep) {
@@ -960,8 +1052,12 @@ int uot_generate_problem(uot_ctx* ctx, uint64_t seed, double er, double ep) {
   ctx->ep = ep;
   ctx->have_problem = false;
   const unsigned gblocks = static_cast<unsigned>(ctx->sms) * 16;
-  gen_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->P, seed, ctx->row_offset, ctx->rows,
-                                                     static_cast<unsigned>(ctx->cols), ctx->pitch);
+  if (ctx->dtype == UOT_F64)
+    gen_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(static_cast<double*>(ctx->P), seed, ctx->row_offset,
+                                                       ctx->rows, static_cast<unsigned>(ctx->cols), ctx->pitch);
+  else
+    gen_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->Pf(), seed, ctx->row_offset, ctx->rows,
+                                                       static_cast<unsigned>(ctx->cols), ctx->pitch);
   gen_marginals_kernel<<<gblocks, 256, 0, ctx->stream>>>(ctx->rpd, ctx->cpd, seed, ctx->global_rows,
                                                          ctx->row_offset, ctx->rows,
                                                          static_cast<unsigned>(ctx->cols));
@@ -983,11 +1079,14 @@ int uot_set_fi(uot_ctx* ctx, double fi) {
 
 int uot_set_plan(uot_ctx* ctx, const float* a) {
   if (!ctx || !a) return UOT_INVALID_PARAMETER;
-  if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
-  CK(cudaSetDevice(ctx->device));
-  CK(cudaMemcpy2DAsync(ctx->P, ctx->pitch * sizeof(float), a, ctx->cols * sizeof(float),
-                       ctx->cols * sizeof(float), ctx->rows, cudaMemcpyHostToDevice, ctx->stream));
-  return after_matrix_upload(ctx);
+  int rc = dtype_check(ctx, UOT_F32, "uot_set_plan");
+  return rc ? rc : set_plan_any(ctx, a);
+}
+
+int uot_set_plan_f64(uot_ctx* ctx, const double* a) {
+  if (!ctx || !a) return UOT_INVALID_PARAMETER;
+  int rc = dtype_check(ctx, UOT_F64, "uot_set_plan_f64");
+  return rc ? rc : set_plan_any(ctx, a);
 }
 
 int uot_init_col_sums(uot_ctx* ctx) {
@@ -1142,11 +1241,15 @@ int uot_get_factors(const uot_ctx* cctx, double* alpha, double* beta) {
 int uot_get_plan(const uot_ctx* cctx, float* out) {
   auto* ctx = const_cast<uot_ctx*>(cctx);
   if (!ctx || !out) return UOT_INVALID_PARAMETER;
-  CK(cudaSetDevice(ctx->device));
-  CK(cudaMemcpy2DAsync(out, ctx->cols * sizeof(float), ctx->P, ctx->pitch * sizeof(float),
-                       ctx->cols * sizeof(float), ctx->rows, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  return UOT_OK;
+  int rc = dtype_check(ctx, UOT_F32, "uot_get_plan");
+  return rc ? rc : get_plan_any(ctx, out);
+}
+
+int uot_get_plan_f64(const uot_ctx* cctx, double* out) {
+  auto* ctx = const_cast<uot_ctx*>(cctx);
+  if (!ctx || !out) return UOT_INVALID_PARAMETER;
+  int rc = dtype_check(ctx, UOT_F64, "uot_get_plan_f64");
+  return rc ? rc : get_plan_any(ctx, out);
 }
 
 int uot_get_report(const uot_ctx* ctx, uint64_t* iterations, double* final_error, int* converged) {
@@ -1252,6 +1355,31 @@ int uot_gen_block_f32(uint64_t seed, uint64_t global_rows, uint64_t n, uint64_t 
   for (int t = 0; t < nt; ++t)
     th.emplace_back([&, t] {
       for (uint64_t k = mn * t / nt; k < mn * (t + 1) / nt; ++k) a[k] = static_cast<float>(unit_at(first + k));
+    });
+  for (auto& x : th) x.join();
+  if (rpd)
+    for (uint64_t i = 0; i < rows; ++i) rpd[i] = unit_at(gmn + row0 + i);
+  if (cpd)
+    for (uint64_t j = 0; j < n; ++j) cpd[j] = unit_at(gmn + global_rows + j);
+  return UOT_OK;
+}
+
+int uot_gen_block_f64(uint64_t seed, uint64_t global_rows, uint64_t n, uint64_t row0, uint64_t rows,
+                      double* a, double* rpd, double* cpd, int threads) {  // gen_problem_t<double>
+  if (global_rows < 1 || n < 1 || row0 + rows > global_rows) return UOT_INVALID_PARAMETER;
+  auto unit_at = [seed](uint64_t k) {
+    uint64_t z = seed + (k + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return static_cast<double>((z >> 11) + 1) * 0x1p-53;
+  };
+  const uint64_t mn = rows * n, first = row0 * n, gmn = global_rows * n;
+  const int nt = std::max(1, std::min<int>(threads, 256));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (uint64_t k = mn * t / nt; k < mn * (t + 1) / nt; ++k) a[k] = unit_at(first + k);
     });
   for (auto& x : th) x.join();
   if (rpd)
@@ -1374,7 +1502,7 @@ struct Staging {
     }
   }
   int init(uot_ctx* ctx) {
-    const uint64_t row_bytes = ctx->cols * 4;
+    const uint64_t row_bytes = ctx->cols * ctx->esz;
     rows_per = std::max<uint64_t>(1, (64ull << 20) / row_bytes);
     rows_per = std::min<uint64_t>(rows_per, ctx->rows);
     for (int i = 0; i < 2; ++i) {
@@ -1415,13 +1543,14 @@ int uot_load_problem_file(uot_ctx* ctx, const char* path) {
   if (f.fd < 0) return ctx->fail(UOT_IO_ERROR, "read_problem: cannot open %s", path);
   UotpHeader h;
   if (read_uotp_header(f.fd, path, &h)) return ctx->fail(UOT_IO_ERROR, "%s", g_io_error.c_str());
-  if (h.dtype != UOT_F32)
-    return ctx->fail(UOT_INVALID_PARAMETER, "%s holds a Problem<double>: only f32 has an sm_100a kernel", path);
+  if (h.dtype != ctx->dtype)
+    return ctx->fail(UOT_INVALID_PARAMETER, "%s holds a Problem<%s>, the session a Problem<%s>", path,
+                     h.dtype == UOT_F64 ? "double" : "float", ctx->dtype == UOT_F64 ? "double" : "float");
   if (h.m != ctx->global_rows || h.n != ctx->cols)
     return ctx->fail(UOT_INVALID_PARAMETER, "%s is %llux%llu, the session expects %llux%llu", path,
                      (unsigned long long)h.m, (unsigned long long)h.n, (unsigned long long)ctx->global_rows,
                      (unsigned long long)ctx->cols);
-  const uint64_t mat_off = kUotpHeader, rpd_off = mat_off + h.m * h.n * 4, cpd_off = rpd_off + 8 * h.m;
+  const uint64_t mat_off = kUotpHeader, rpd_off = mat_off + h.m * h.n * h.elem, cpd_off = rpd_off + 8 * h.m;
   std::vector<double> rpd(ctx->rows), cpd(ctx->cols);
   if (!pread_all(f.fd, rpd.data(), 8 * ctx->rows, rpd_off + 8 * ctx->row_offset) ||
       !pread_all(f.fd, cpd.data(), 8 * ctx->cols, cpd_off))
@@ -1433,15 +1562,15 @@ int uot_load_problem_file(uot_ctx* ctx, const char* path) {
   ctx->have_problem = false;
   Staging sg;
   if ((rc = sg.init(ctx))) return rc;
-  const uint64_t row_bytes = ctx->cols * 4;
+  const uint64_t row_bytes = ctx->cols * ctx->esz;
   for (uint64_t r0 = 0, k = 0; r0 < ctx->rows; r0 += sg.rows_per, ++k) {
     const uint64_t nr = std::min<uint64_t>(sg.rows_per, ctx->rows - r0);
     const int i = static_cast<int>(k & 1);
     CK(cudaEventSynchronize(sg.ev[i]));  // the copy out of this buffer two chunks ago is done
     if (!pread_all(f.fd, sg.buf[i], nr * row_bytes, mat_off + (ctx->row_offset + r0) * row_bytes))
       return ctx->fail(UOT_IO_ERROR, "read_problem: short read from %s", path);
-    CK(cudaMemcpy2DAsync(ctx->P + r0 * ctx->pitch, ctx->pitch * sizeof(float), sg.buf[i], row_bytes, row_bytes, nr,
-                         cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpy2DAsync(static_cast<char*>(ctx->P) + r0 * ctx->pitch * ctx->esz, ctx->pitch * ctx->esz, sg.buf[i],
+                         row_bytes, row_bytes, nr, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaEventRecord(sg.ev[i], ctx->stream));
   }
   CK(cudaMemcpyAsync(ctx->rpd, rpd.data(), ctx->rows * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -1461,14 +1590,14 @@ int uot_save_problem_file(uot_ctx* ctx, const char* path) {
   f.fd = open(path, O_WRONLY | O_CREAT, 0644);  // every rank opens; no truncation races
   if (f.fd < 0) return ctx->fail(UOT_IO_ERROR, "write_problem: cannot open %s", path);
   const uint64_t m = ctx->global_rows, n = ctx->cols;
-  const uint64_t mat_off = kUotpHeader, rpd_off = mat_off + m * n * 4, cpd_off = rpd_off + 8 * m;
+  const uint64_t mat_off = kUotpHeader, rpd_off = mat_off + m * n * ctx->esz, cpd_off = rpd_off + 8 * m;
   if (ftruncate(f.fd, static_cast<off_t>(cpd_off + 8 * n)) != 0)
     return ctx->fail(UOT_IO_ERROR, "write_problem: cannot size %s", path);
   if (ctx->rank == 0) {
     unsigned char b[kUotpHeader];
     std::memcpy(b, "UOTP", 4);
     put_le(b + 4, 1, 2);
-    put_le(b + 6, UOT_F32, 2);
+    put_le(b + 6, static_cast<uint64_t>(ctx->dtype), 2);
     put_le(b + 8, m, 8);
     put_le(b + 16, n, 8);
     uint64_t er, ep;
@@ -1487,7 +1616,7 @@ int uot_save_problem_file(uot_ctx* ctx, const char* path) {
   Staging sg;
   int rc = sg.init(ctx);
   if (rc) return rc;
-  const uint64_t row_bytes = n * 4;
+  const uint64_t row_bytes = n * ctx->esz;
   uint64_t pend_r0[2] = {0, 0}, pend_nr[2] = {0, 0};
   auto flush = [&](int i) -> bool {
     if (!pend_nr[i]) return true;
@@ -1500,8 +1629,8 @@ int uot_save_problem_file(uot_ctx* ctx, const char* path) {
     const uint64_t nr = std::min<uint64_t>(sg.rows_per, ctx->rows - r0);
     const int i = static_cast<int>(k & 1);
     if (!flush(i)) return ctx->fail(UOT_IO_ERROR, "write_problem: short write to %s", path);
-    CK(cudaMemcpy2DAsync(sg.buf[i], row_bytes, ctx->P + r0 * ctx->pitch, ctx->pitch * sizeof(float), row_bytes, nr,
-                         cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpy2DAsync(sg.buf[i], row_bytes, static_cast<const char*>(ctx->P) + r0 * ctx->pitch * ctx->esz,
+                         ctx->pitch * ctx->esz, row_bytes, nr, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaEventRecord(sg.ev[i], ctx->stream));
     pend_r0[i] = r0;
     pend_nr[i] = nr;

@@ -88,7 +88,7 @@ class Layout(C.Structure):
                 ("nbuf", C.c_uint32), ("sms", C.c_uint32), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("device", C.c_int32), ("evict_first", C.c_int32),
                 ("smid_map", C.c_int32), ("exchange", C.c_int32), ("tmem", C.c_int32),
-                ("resident", C.c_int32), ("persist", C.c_int32)]
+                ("resident", C.c_int32), ("persist", C.c_int32), ("dtype", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -135,6 +135,10 @@ def lib():
     L.uot_get_stream.argtypes = [_P]
     L.uot_get_stream.restype = _P
     L.uot_set_problem.argtypes = [_P, _P, _P, _P, _d, _d]
+    L.uot_set_problem_f64.argtypes = [_P, _P, _P, _P, _d, _d]
+    L.uot_set_plan_f64.argtypes = [_P, _P]
+    L.uot_get_plan_f64.argtypes = [_P, _P]
+    L.uot_gen_block_f64.argtypes = [_u64, _u64, _u64, _u64, _u64, _P, _P, _P, _i]
     L.uot_generate_problem.argtypes = [_P, _u64, _d, _d]
     L.uot_set_plan.argtypes = [_P, _P]
     L.uot_set_fi.argtypes = [_P, _d]
@@ -284,30 +288,29 @@ class PinnedBuffer:
 
 
 def gen_block(seed: int, global_rows: int, n: int, row0: int, rows: int, threads: int = 0,
-              out: np.ndarray | None = None) -> Problem:
-    """Rows [row0, row0+rows) of gen_problem_t<float>(seed, global_rows, n): the
-    rank-local block of a row-sharded problem (A block, rpd slice, full cpd)."""
-    a = np.empty((rows, n), np.float32) if out is None else out
+              out: np.ndarray | None = None, dtype=np.float32) -> Problem:
+    """Rows [row0, row0+rows) of gen_problem_t<T>(seed, global_rows, n) (T = float
+    or double): the rank-local block of a row-sharded problem (A block, rpd
+    slice, full cpd)."""
+    dtype = np.dtype(dtype) if out is None else out.dtype
+    a = np.empty((rows, n), dtype) if out is None else out
     rpd = np.empty(rows, np.float64)
     cpd = np.empty(n, np.float64)
-    rc = lib().uot_gen_block_f32(int(seed), int(global_rows), int(n), int(row0), int(rows), _ptr(a),
-                                 _ptr(rpd), _ptr(cpd), threads or (os.cpu_count() or 1))
+    fn = lib().uot_gen_block_f64 if dtype == np.float64 else lib().uot_gen_block_f32
+    rc = fn(int(seed), int(global_rows), int(n), int(row0), int(rows), _ptr(a), _ptr(rpd), _ptr(cpd),
+            threads or (os.cpu_count() or 1))
     if rc:
         _raise(rc, "gen_block: bad block")
     return Problem(a, rpd, cpd, 1.0, 1.0)
 
 
-def gen_problem_t(seed: int, m: int, n: int, threads: int = 0, out: np.ndarray | None = None) -> Problem:
-    """gen_problem_t<float> (problem_io.hpp:17-31); er = ep = 1. `out` may be a
-    preallocated (m, n) float32 array (e.g. PinnedBuffer.array)."""
+def gen_problem_t(seed: int, m: int, n: int, threads: int = 0, out: np.ndarray | None = None,
+                  dtype=np.float32) -> Problem:
+    """gen_problem_t<T> (problem_io.hpp:17-31), T = float (default) or double;
+    er = ep = 1. `out` may be a preallocated (m, n) array (e.g. PinnedBuffer.array)."""
     if m < 1 or n < 1:
         _raise(1, "gen_problem: matrix must be at least 1x1")
-    a = np.empty((m, n), np.float32) if out is None else out
-    rpd = np.empty(m, np.float64)
-    cpd = np.empty(n, np.float64)
-    lib().uot_gen_problem_f32(int(seed), m, n, _ptr(a), _ptr(rpd), _ptr(cpd),
-                              threads or (os.cpu_count() or 1))
-    return Problem(a, rpd, cpd, 1.0, 1.0)
+    return gen_block(seed, m, n, 0, m, threads, out, dtype)
 
 
 # ---------------------------------------------------------- problem files --
@@ -325,22 +328,24 @@ def problem_file_info(path) -> dict:
 
 
 def read_problem(path) -> Problem:
-    """read_problem (problem_io.cpp:106-141) on the host for an f32 file."""
+    """read_problem (problem_io.cpp:106-141) on the host: a Problem<float> or
+    Problem<double> (the matrix dtype says which)."""
     info = problem_file_info(path)
-    if info["dtype"] != "f32":
-        _raise(1, f"{path} holds a Problem<double>: only f32 has an sm_100a kernel")
     m, n = info["m"], info["n"]
+    es, code = (8, "<f8") if info["dtype"] == "f64" else (4, "<f4")
     raw = np.fromfile(path, dtype=np.uint8, offset=40)
-    a = raw[: 4 * m * n].view("<f4").reshape(m, n)
-    rpd = raw[4 * m * n: 4 * m * n + 8 * m].view("<f8")
-    cpd = raw[4 * m * n + 8 * m:].view("<f8")
-    return Problem(a.astype(np.float32), rpd.astype(np.float64), cpd.astype(np.float64), info["er"], info["ep"])
+    a = raw[: es * m * n].view(code).reshape(m, n)
+    rpd = raw[es * m * n: es * m * n + 8 * m].view("<f8")
+    cpd = raw[es * m * n + 8 * m:].view("<f8")
+    dt = np.float64 if es == 8 else np.float32
+    return Problem(a.astype(dt), rpd.astype(np.float64), cpd.astype(np.float64), info["er"], info["ep"])
 
 
 def write_problem(path, p: Problem):
-    """write_problem (problem_io.cpp:97-104) of a Problem<float> from host memory."""
-    a = np.ascontiguousarray(p.a, "<f4")
-    hdr = bytearray(b"UOTP") + (1).to_bytes(2, "little") + (1).to_bytes(2, "little")
+    """write_problem (problem_io.cpp:97-104) of a Problem<float> or Problem<double>."""
+    f64 = np.asarray(p.a).dtype == np.float64
+    a = np.ascontiguousarray(p.a, "<f8" if f64 else "<f4")
+    hdr = bytearray(b"UOTP") + (1).to_bytes(2, "little") + (2 if f64 else 1).to_bytes(2, "little")
     hdr += int(a.shape[0]).to_bytes(8, "little") + int(a.shape[1]).to_bytes(8, "little")
     hdr += np.array([p.er, p.ep], "<f8").tobytes()
     with open(path, "wb") as f:
@@ -360,19 +365,24 @@ class Session:
     set_problem -> init_col_sums -> iterate(k, tol) -> factors()/plan().
     """
 
-    def __init__(self, rows: int, cols: int, device: int = 0, *, dist=None):
+    def __init__(self, rows: int, cols: int, device: int = 0, *, dist=None, dtype=np.float32):
+        """dtype: np.float32 (Problem<float>) or np.float64 (Problem<double>)."""
         self._h = _P()
         L = lib()
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in (np.float32, np.float64):
+            _raise(1, f"dtype {self.dtype}: Problem<float> or Problem<double> only")
+        code = UOT_F64 if self.dtype == np.float64 else UOT_F32
         if dist is None:
-            rc = L.uot_create(C.byref(self._h), int(rows), int(cols), UOT_F32, int(device))
+            rc = L.uot_create(C.byref(self._h), int(rows), int(cols), code, int(device))
         elif dist[2] == "peer":  # (rank, nranks, "peer"): connect() with every rank's handle next
             rank, nranks, _ = dist
-            rc = L.uot_create_peer(C.byref(self._h), int(rows), int(cols), UOT_F32, int(device),
+            rc = L.uot_create_peer(C.byref(self._h), int(rows), int(cols), code, int(device),
                                    int(rank), int(nranks))
         else:
             rank, nranks, nccl_id = dist
             idbuf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id).ljust(128, b"\0"))
-            rc = L.uot_create_dist(C.byref(self._h), int(rows), int(cols), UOT_F32, int(device),
+            rc = L.uot_create_dist(C.byref(self._h), int(rows), int(cols), code, int(device),
                                    int(rank), int(nranks), C.cast(idbuf, _P))
         if rc:
             msg = self._err()
@@ -416,7 +426,7 @@ class Session:
 
     # -- problem
     def set_problem(self, p: Problem):
-        a = np.ascontiguousarray(p.a, np.float32)
+        a = np.ascontiguousarray(p.a, self.dtype)
         if a.shape != (self.rows, self.cols):
             _raise(1, f"matrix shape {a.shape} does not match the session ({self.rows}, {self.cols})")
         rpd = np.ascontiguousarray(p.rpd, np.float64)
@@ -425,7 +435,8 @@ class Session:
             _raise(1, f"row-marginal length {rpd.size} does not match row count {self.rows}")
         if cpd.size != self.cols:
             _raise(1, f"column-marginal length {cpd.size} does not match column count {self.cols}")
-        self._check(lib().uot_set_problem(self._h, _ptr(a), _ptr(rpd), _ptr(cpd), float(p.er), float(p.ep)))
+        fn = lib().uot_set_problem_f64 if self.dtype == np.float64 else lib().uot_set_problem
+        self._check(fn(self._h, _ptr(a), _ptr(rpd), _ptr(cpd), float(p.er), float(p.ep)))
 
     def load_problem_file(self, path):
         """read_problem (problem_io.cpp:106-141) of this session's row block,
@@ -444,10 +455,11 @@ class Session:
         self._check(lib().uot_generate_problem(self._h, int(seed), float(er), float(ep)))
 
     def set_plan(self, a: np.ndarray):
-        a = np.ascontiguousarray(a, np.float32)
+        a = np.ascontiguousarray(a, self.dtype)
         if a.shape != (self.rows, self.cols):
             _raise(1, "fused_iterate: matrix shape does not match problem")
-        self._check(lib().uot_set_plan(self._h, _ptr(a)))
+        fn = lib().uot_set_plan_f64 if self.dtype == np.float64 else lib().uot_set_plan
+        self._check(fn(self._h, _ptr(a)))
 
     # -- the path
     def init_col_sums(self):
@@ -488,8 +500,11 @@ class Session:
 
     def plan(self, out: np.ndarray | None = None) -> np.ndarray:
         if out is None:
-            out = np.empty((self.rows, self.cols), np.float32)
-        self._check(lib().uot_get_plan(self._h, _ptr(out)))
+            out = np.empty((self.rows, self.cols), self.dtype)
+        if out.dtype != self.dtype or out.shape != (self.rows, self.cols) or not out.flags.c_contiguous:
+            _raise(1, f"plan buffer must be a C-contiguous {self.dtype} array of shape ({self.rows}, {self.cols})")
+        fn = lib().uot_get_plan_f64 if self.dtype == np.float64 else lib().uot_get_plan
+        self._check(fn(self._h, _ptr(out)))
         return out
 
     def report(self):
@@ -542,7 +557,8 @@ def fused_solve(p: Problem, tol: float, max_iter: int, device: int = 0,
     _validate_controls(tol, max_iter, "fused_solve")
     t0 = time.perf_counter()
     own = session is None
-    s = Session(p.m(), p.n(), device) if own else session
+    dt = np.float64 if np.asarray(p.a).dtype == np.float64 else np.float32  # Problem<double> stays double
+    s = Session(p.m(), p.n(), device, dtype=dt) if own else session
     try:
         s.set_problem(p)
         s.init_col_sums()

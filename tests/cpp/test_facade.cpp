@@ -182,6 +182,20 @@ void test_problem_files_round_trip() {  // problem_io.cpp:97-141
   std::filesystem::remove(out);
 }
 
+void test_f64_problem_matches_reference() {  // Problem<double>, Dtype::f64
+  auto p = uot::gen_problem_t<double>(44, 300, 700);
+  p.er = 1.0;
+  p.ep = 0.25;
+  const auto ref = uot::fused_solve(p, kNever, 15, std::size_t(4));
+  const auto gpu = uot::cuda::fused_solve(p, kNever, 15);
+  CHECK(gpu.report.iterations == 15);
+  double m = 0.0;
+  for (std::size_t k = 0; k < gpu.plan.size(); ++k)
+    m = std::max(m, std::abs(gpu.plan.data()[k] - ref.plan.data()[k]) / ref.plan.data()[k]);
+  CHECK(m <= 1e-12);
+  CHECK(uot::max_abs_diff(gpu.factors.beta, ref.factors.beta) <= 1e-12);
+}
+
 void test_single_rank_peer_distributed() {
   const auto p = random_problem(25, 64, 64, 0.5);
   const auto d = uot::cuda::distributed_solve_peer(p, kNever, 11, 0, 1, 0,
@@ -205,6 +219,7 @@ int main() {
       {"ablation solvers", test_ablation_solvers_match_reference},
       {"problem files", test_problem_files_round_trip},
       {"single-rank peer distributed", test_single_rank_peer_distributed},
+      {"Problem<double>", test_f64_problem_matches_reference},
   };
   for (const auto& [name, fn] : cases) {
     const int before = g_fail;

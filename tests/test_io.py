@@ -43,11 +43,23 @@ def test_write_is_byte_identical_to_the_reference(uot, orc, tmp_path, name, seed
     assert out.read_bytes() == open(os.path.join(GOLDEN, name), "rb").read()
 
 
-def test_f64_container_header(uot):
-    info = uot.problem_file_info(os.path.join(GOLDEN, "io_2x2_f64.uotp"))
+def test_f64_container(uot, orc):
+    # a Problem<double> container written by the reference (make_uotp.py: the
+    # seed-5 2x2 fp32 draw widened to double)
+    path = os.path.join(GOLDEN, "io_2x2_f64.uotp")
+    info = uot.problem_file_info(path)
     assert info["dtype"] == "f64" and (info["m"], info["n"]) == (2, 2)
-    with pytest.raises(uot.InvalidParameter):
-        uot.read_problem(os.path.join(GOLDEN, "io_2x2_f64.uotp"))
+    p = uot.read_problem(path)
+    a, rpd, cpd = orc.gen_problem(5, 2, 2)
+    assert p.a.dtype == np.float64 and np.array_equal(p.a, a.astype(np.float64))
+    assert np.array_equal(p.rpd, rpd) and np.array_equal(p.cpd, cpd) and p.ep == 0.25
+
+
+def test_f64_write_is_byte_identical(uot, orc, tmp_path):
+    a, rpd, cpd = orc.gen_problem(5, 2, 2)
+    out = tmp_path / "f64.uotp"
+    uot.write_problem(out, uot.Problem(a.astype(np.float64), rpd, cpd, 1.0, 0.25))
+    assert out.read_bytes() == open(os.path.join(GOLDEN, "io_2x2_f64.uotp"), "rb").read()
 
 
 def test_malformed_containers_raise_ioerror(uot, tmp_path):
