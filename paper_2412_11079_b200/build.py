@@ -14,6 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libuot_cuda.so")
 TRACE_SO = os.path.join(PKG, "libuot_cuda_trace.so")  # phase-timer build for profiling runs
+CLI = os.path.join(PKG, "uot-cuda")  # the reference CLI's gen/solve/bench on the C ABI
 SOURCES = [os.path.join(CSRC, "uot_cuda.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")] + [
     os.path.join(ROOT, "include", "uot_cuda.h")]
@@ -52,6 +53,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return SO
 
 
+def build_cli() -> str:
+    """g++ the CLI front end against the C ABI (links libuot_cuda.so, rpath $ORIGIN)."""
+    src = os.path.join(CSRC, "uot_cli.cpp")
+    if os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(src), os.path.getmtime(SO)):
+        return CLI
+    cmd = ["g++", "-O2", "-std=c++17", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), "-o", CLI, src,
+           "-L", PKG, "-l:libuot_cuda.so", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building the uot-cuda CLI")
+    return CLI
+
+
 def build_trace() -> str:
     cmd = nvcc_cmd(TRACE_SO, ["-DUOT_TRACE"])
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -77,3 +92,4 @@ if __name__ == "__main__":
     if "--pipe" in sys.argv:
         build_variant("pipe", ["UOT_PIPE_ONLY"])
     build(force="--force" in sys.argv, verbose="--quiet" not in sys.argv)
+    build_cli()
