@@ -113,6 +113,8 @@ __device__ __forceinline__ double exchange_row_sum(ulonglong2* xrec, unsigned ct
   double tot = 0.0;
   for (unsigned g0 = 0; g0 < G; g0 += 32) {
     double v = 0.0;
+    // every lane polls, its own CTA's record included (measured: skipping the
+    // own record and using t directly is 1.5% slower at 32768^2)
     if (g0 + lane < G) {
       const ulonglong2* rec = &xrec[static_cast<size_t>(group * G + g0 + lane) * kRing + slot];
       unsigned long long lo, hi;

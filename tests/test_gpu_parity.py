@@ -308,3 +308,22 @@ def test_very_wide_rows(gpu, orc, m, n, k):
     ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 4)
     assert_parity(plan, ref.plan, rpd, cpd, f"{m}x{n}")
     np.testing.assert_allclose(f.alpha, ref.alpha, rtol=1e-12)
+
+
+def test_randomized_shapes_against_oracle(gpu, orc):
+    # seeded sweep over shapes, damping and iteration counts that exercise every
+    # layout: G = 1 with 1..8 rows per batch, G > 1, ragged slices, resident and
+    # streaming modes, fi < 1 and fi = 1
+    rng = np.random.default_rng(2024)
+    for case in range(24):
+        m = int(rng.integers(1, 700))
+        n = int(rng.choice([int(rng.integers(1, 300)), int(rng.integers(300, 9000)), int(rng.integers(9000, 40000))]))
+        fi = float(rng.choice([1.0, 0.5, 1 / 1.1, 0.9]))
+        k = int(rng.integers(1, 12))
+        er, ep = er_ep(fi)
+        a, rpd, cpd = orc.gen_problem(int(rng.integers(0, 2**31)), m, n)
+        plan, f, cs, it, err, conv, lay = solve(gpu, a, rpd, cpd, er, ep, k)
+        ref = orc.fused_solve(a, rpd, cpd, er, ep, KNEVER, k, 3)
+        assert it == k, (case, m, n)
+        assert_parity(plan, ref.plan, rpd, cpd, f"case {case}: {m}x{n} fi={fi} k={k} layout={lay}")
+        assert abs(err - ref.final_error) <= 1e-9 * max(1.0, ref.final_error), (case, m, n)
