@@ -118,6 +118,7 @@ class Session {
   }
   // UOT_VARIANT_FUSED (default), UOT_VARIANT_TWO_PASS (tiled.hpp), UOT_VARIANT_BASELINE (baseline.hpp).
   void set_variant(int variant) { check(uot_set_variant(ctx_, variant)); }
+  void set_deterministic(bool on) { check(uot_set_deterministic(ctx_, on ? 1 : 0)); }
   void set_plan(const Matrix<float>& a) { check(uot_set_plan(ctx_, a.data().data())); }
   void init_col_sums() { check(uot_init_col_sums(ctx_)); }
   void set_state(const FusedState& st) { check(uot_set_col_sums(ctx_, st.col_sums.data())); }

@@ -74,6 +74,7 @@ typedef struct uot_layout {
   int32_t resident;      /* uot_iterate runs as ONE persistent launch, matrix in shared memory (resident.cuh) */
   int32_t persist;       /* otherwise, single rank: ONE persistent streaming launch (persist.cuh) */
   int32_t dtype;         /* UOT_F32 (Problem<float>) or UOT_F64 (Problem<double>) */
+  int32_t dynamic;       /* 1: row batches handed out by a device counter (uot_set_deterministic) */
 } uot_layout;
 
 /* ---- sessions ---------------------------------------------------------- */
@@ -133,6 +134,14 @@ UOT_API int uot_save_problem_file(uot_ctx* ctx, const char* path);
 #define UOT_VARIANT_TWO_PASS 1
 #define UOT_VARIANT_BASELINE 2
 UOT_API int uot_set_variant(uot_ctx* ctx, int variant);
+
+/* Row-batch schedule of the fused sweep. Default (0): batches go to whichever
+ * CTA asks next (a device counter), so SMs with more HBM bandwidth take more
+ * rows; the f64 column sums then add rows in a run-dependent order (results
+ * agree to ~1e-12 relative between runs). 1: every row group owns a fixed
+ * contiguous row block (balanced_blocks, plan.cpp:11-21): bit-reproducible
+ * run to run, slower where per-SM bandwidth differs. */
+UOT_API int uot_set_deterministic(uot_ctx* ctx, int on);
 
 UOT_API void uot_destroy(uot_ctx* ctx);
 UOT_API const char* uot_last_error(const uot_ctx* ctx);

@@ -89,7 +89,8 @@ def build_variant(name: str, defines: list[str]) -> str:
 if __name__ == "__main__":
     if "--trace" in sys.argv:
         build_trace()
-    if "--pipe" in sys.argv:
-        build_variant("pipe", ["UOT_PIPE_ONLY"])
+    if "--exp" in sys.argv:  # power / pipeline attribution builds (UOT_EXP in sweep.cuh)
+        build_variant("exp1", ["UOT_EXP=1"])
+        build_variant("exp2", ["UOT_EXP=2"])
     build(force="--force" in sys.argv, verbose="--quiet" not in sys.argv)
     build_cli()

@@ -230,6 +230,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
   }
   if (threadIdx.x != 0) return;
   ctl->fin_count = 0;
+  ctl->batch_next = 0;  // the sweep before this finalize has retired
+  ctl->sweep_seq += 1;
   if (XCH != kXchNone && !REDUCE && MODE != kFinBetaOnly) ctl->xseq = seq;
   ctl->beta_bad = ctl->beta_bad_next;
   ctl->beta_bad_next = 0;

@@ -93,6 +93,7 @@ __global__ void reset_control_kernel(Control* c) {
   c->beta_bad_next = 0;
   c->alpha_bad = 0;
   c->fin_count = 0;
+  c->batch_next = 0;
 }
 
 // Start of an iterate() call: new tolerance; a failed session stays stopped.
@@ -100,6 +101,7 @@ __global__ void begin_iterate_kernel(Control* c, double tol) {
   c->tol = tol;
   c->converged = 0;
   c->done = c->status != 0 ? 1 : 0;
+  c->batch_next = 0;
 }
 
 }  // namespace uotk

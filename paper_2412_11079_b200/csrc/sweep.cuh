@@ -61,6 +61,8 @@ struct SweepArgs {
   unsigned int buf_stride;    // bytes per smem ring slot (128-aligned, >= B*slice*4)
   int evict_first;            // stream P past L2 (problem larger than L2)
   int smid_map;               // CTA slot = %smid (the grid covers every SM exactly once)
+  int dyn;                    // batches handed out by a global counter (else a static row block)
+  ulonglong2* mail;           // [groups][kMail] {first row, tag}: the group leader's batch picks (dyn, G > 1)
   double fi;
 };
 
@@ -92,6 +94,8 @@ __host__ __device__ constexpr int tr_slot(int id) {
 
 constexpr int kRing = 8;   // exchange records per CTA
 constexpr int kQ = 4;      // ring depth of row partials / factors handed between roles
+constexpr int kMail = 32;  // batch picks a group leader publishes ahead of its followers
+constexpr unsigned long long kNoRow = ~0ull;  // ring slot sentinel: no batch left
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -125,6 +129,10 @@ __device__ __forceinline__ double exchange_row_sum(ulonglong2* xrec, unsigned ct
         do {
           ld_relaxed_b128(rec, lo, hi);
           if (hi != tag && (++n & 255u) == 0 && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
+#ifdef UOT_DEBUG
+            printf("xchg timeout cta %u group %u slot %u tag %llx seen %llx (rec of cta %u)\n", cta, group, slot, tag, hi,
+                   group * G + g0 + lane);
+#endif
             atomicOr(&ctl->status, kStatusExchangeTimeout);
             break;
           }
@@ -215,10 +223,11 @@ __device__ __forceinline__ void group_sweep1(float4* row, float4 (&v)[KG], uint3
     for (int kk = 0; kk < KG; ++kk)
 #pragma unroll
       for (int e = 0; e < 4; ++e) comp(v[kk], e) = d2f(fastd(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
+    const bool ok0 = FULL || tid + g0 * NT < nq;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) t[e] = 0.0;
+    for (int e = 0; e < 4; ++e) t[e] = ok0 ? fastd(comp(v[0], e)) : 0.0;  // (no 0.0 + x DADD)
 #pragma unroll
-    for (int kk = 0; kk < KG; ++kk)
+    for (int kk = 1; kk < KG; ++kk)
       if (FULL || tid + (g0 + kk) * NT < nq)
 #pragma unroll
         for (int e = 0; e < 4; ++e) t[e] += fastd(comp(v[kk], e));
@@ -229,10 +238,11 @@ __device__ __forceinline__ void group_sweep1(float4* row, float4 (&v)[KG], uint3
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         comp(v[kk], e) = d2f(static_cast<double>(comp(v[kk], e)) * beta[4 * (g0 + kk) + e]);
+    const bool ok0 = FULL || tid + g0 * NT < nq;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) t[e] = 0.0;
+    for (int e = 0; e < 4; ++e) t[e] = ok0 ? static_cast<double>(comp(v[0], e)) : 0.0;
 #pragma unroll
-    for (int kk = 0; kk < KG; ++kk)
+    for (int kk = 1; kk < KG; ++kk)
       if (FULL || tid + (g0 + kk) * NT < nq)
 #pragma unroll
         for (int e = 0; e < 4; ++e) t[e] += static_cast<double>(comp(v[kk], e));
@@ -297,6 +307,67 @@ __device__ __forceinline__ double row_sweep1(float4* row, unsigned tid, unsigned
     const uint32_t m = screen_group<KG>(v, sb.lo);
     double t[4];
     group_sweep1<NT, KG, FULL>(row, v, m, g0, tid, nq, beta, sb, t, bad);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[e] = g0 == 0 ? t[e] : s[e] + t[e];
+  }
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+// ---- column factors parked in TMEM (TB builds) ----------------------------
+// A compute thread's 4V column factors (f64, two 32-bit TMEM columns each) sit
+// in its own TMEM lane: warp w owns lanes 32*(w%4).. and 8V columns from
+// 8V*(w/4). Sweep 1 loads a chunk group's factors right before use, which frees
+// the 8V registers the factors otherwise occupy for the whole sweep.
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc_cols(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_dealloc_cols(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+__device__ __forceinline__ void tmem_st_chunk(uint32_t taddr, const double* b) {  // 4 doubles, .x8
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(__double2loint(b[0])), "r"(__double2hiint(b[0])), "r"(__double2loint(b[1])),
+               "r"(__double2hiint(b[1])), "r"(__double2loint(b[2])), "r"(__double2hiint(b[2])),
+               "r"(__double2loint(b[3])), "r"(__double2hiint(b[3]))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld_chunk(uint32_t taddr, double* b) {  // 4 doubles, .x8 (no wait)
+  int w[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "r"(taddr)
+               : "memory");
+#pragma unroll
+  for (int e = 0; e < 4; ++e) b[e] = __hiloint2double(w[2 * e + 1], w[2 * e]);
+}
+__device__ __forceinline__ void tmem_wait_ld_() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st_() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_before_() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after_() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Sweep 1 with the factors of each chunk group loaded from TMEM (tcol: this
+// thread's first factor column).
+template <int NT, int V, bool FULL>
+__device__ __forceinline__ double row_sweep1_tb(float4* row, unsigned tid, unsigned nq, uint32_t tcol,
+                                                ScreenBounds sb, bool& bad) {
+  constexpr int KG = ChunkGroup<V>::KG;  // (KG = 4 measured slower: it spills again)
+  double s[4];
+#pragma unroll
+  for (int g0 = 0; g0 < V; g0 += KG) {
+    double bq[4 * V];
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) tmem_ld_chunk(tcol + 8 * (g0 + kk), bq + 4 * (g0 + kk));
+    float4 v[KG];
+    load_group<NT, KG, FULL>(row, v, g0, tid, nq);
+    const uint32_t m = screen_group<KG>(v, sb.lo);
+    tmem_wait_ld_();
+    double t[4];
+    group_sweep1<NT, KG, FULL>(row, v, m, g0, tid, nq, bq, sb, t, bad);
 #pragma unroll
     for (int e = 0; e < 4; ++e) s[e] = g0 == 0 ? t[e] : s[e] + t[e];
   }
@@ -401,6 +472,26 @@ __device__ __forceinline__ void row_seed_f64(const double2* row, unsigned tid, u
   }
 }
 
+// Experiment builds (-DUOT_EXP=1: the compute warps leave the ring untouched,
+// the pipeline alone; 2: they read and write every chunk back, no f64 math).
+#ifndef UOT_EXP
+#define UOT_EXP 0
+#endif
+template <int NT, int V>
+__device__ __forceinline__ void exp_touch(float4* row, unsigned tid) {
+  if (UOT_EXP == 2) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float4 v = row[tid + k * NT];
+      v.x += 0.0f;
+      v.y += 0.0f;
+      v.z += 0.0f;
+      v.w += 0.0f;
+      row[tid + k * NT] = v;
+    }
+  }
+}
+
 // Elements per 16-byte chunk of the storage type.
 template <typename T>
 constexpr int elems_per_chunk() {
@@ -411,7 +502,8 @@ constexpr int elems_per_chunk() {
 template <int NW, int BM, int NBUF>
 struct SweepSmem {
   static constexpr int kBars = NBUF /*full*/ + NBUF /*done2*/ + kQ /*done1*/ + kQ /*alpha_rdy*/;
-  static constexpr int kDoubles = kQ * NW * BM /*red*/ + kQ * BM /*alpha*/;
+  static constexpr int kDoubles = kQ * NW * BM /*red*/ + kQ * BM /*alpha*/ + NBUF /*first row of each slot*/ +
+                                  1 /*TMEM base*/;
   static size_t bytes(unsigned buf_stride) {
     return static_cast<size_t>(NBUF) * buf_stride + kBars * 8 + kDoubles * 8;
   }
@@ -423,10 +515,13 @@ struct SweepSmem {
 // next one (the factor warps' latency budget). XCHG: G > 1, row sums are
 // exchanged across the group. SEED: the read-only init_col_sums sweep. T: the
 // storage type of P (float: Problem<float>, double: Problem<double>).
-template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED, typename T = float>
+template <int NT, int V, int BM, int NBUF, int LA, bool XCHG, int NF, bool FULL, bool SEED, typename T = float,
+          bool TB0 = false>
 __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const SweepArgs a) {
   constexpr int NW = NT / 32;
   constexpr bool F64 = std::is_same<T, double>::value;
+  constexpr bool TB = TB0 && !F64 && !SEED && NW % 4 == 0;  // column factors in TMEM
+  constexpr int kTbCols = (8 * V * (NW / 4) <= 32) ? 32 : (8 * V * (NW / 4) <= 64) ? 64 : (8 * V * (NW / 4) <= 128) ? 128 : 256;
   constexpr int EPC = elems_per_chunk<T>();  // 4 floats or 2 doubles per 16-byte chunk
   static_assert(NF >= 1 && NF <= kErrSlots, "factor warps");
   static_assert(LA >= 1 && LA <= 2 && (!XCHG || LA == 2), "lag (the alpha / red rings hold kQ batches)");
@@ -450,6 +545,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   uint64_t* alpha_rdy = done1 + kQ;
   double* red = reinterpret_cast<double*>(alpha_rdy + kQ);  // [kQ][NW][BM]
   double* alpha_s = red + kQ * NW * BM;                      // [kQ][BM]
+  // first row of the batch in each ring slot (kNoRow: the CTA's batches are
+  // exhausted), written by the producer before the slot's full barrier
+  unsigned long long* srow = reinterpret_cast<unsigned long long*>(alpha_s + kQ * BM);
+  uint32_t* tmem_s = reinterpret_cast<uint32_t*>(srow + NBUF);  // TMEM base (TB)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned G = a.G;
@@ -458,14 +557,19 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   const unsigned cta = a.smid_map ? smid() : blockIdx.x;
   const unsigned group = cta / G, g = cta % G;
   // balanced_blocks over groups (plan.cpp:11-21): first rows%groups get one more.
+  // Row batches. Static: group `group` owns a contiguous block of rows
+  // (balanced_blocks, plan.cpp:11-21). Dynamic: batches of B rows are handed
+  // out by a global counter (ctl->batch_next), so faster SMs take more of
+  // them — per-SM HBM bandwidth on B200 differs by up to 2x with the GPC an SM
+  // sits in (tools/microbench/stream_bench.cu). With G > 1 the group leader
+  // picks and publishes its pick to the followers through `mail`.
+  const unsigned B = a.B;
   const unsigned long long base = a.rows / a.groups, rem = a.rows % a.groups;
   const unsigned long long r0 = group * base + (group < rem ? group : rem);
-  const unsigned nrows = static_cast<unsigned>(base + (group < rem ? 1 : 0));
-  const unsigned B = a.B;
-  const unsigned nb = (nrows + B - 1) / B;
+  const unsigned nb_static = static_cast<unsigned>((base + (group < rem ? 1 : 0) + B - 1) / B);
   const unsigned nq = a.slice / EPC;
   const uint32_t row_bytes = a.slice * static_cast<uint32_t>(sizeof(T));
-  T* gbase = static_cast<T*>(a.P) + r0 * a.pitch + static_cast<size_t>(g) * a.slice;
+  T* gbase = static_cast<T*>(a.P) + static_cast<size_t>(g) * a.slice;
 
   if (tid == 0) {
     for (int i = 0; i < NBUF; ++i) {
@@ -478,12 +582,18 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     }
     fence_mbar_init();
   }
+  if (TB && warp == 0) tmem_alloc_cols<kTbCols>(tmem_s);  // compute warp 0 (warp-collective)
+  if (TB) tmem_fence_before_();
   __syncthreads();
+  if (TB) tmem_fence_after_();
+  const uint32_t tbase = TB ? *tmem_s : 0u;
 
   auto slot_ptr = [&](unsigned b) -> T* {
     return reinterpret_cast<T*>(smem + (b % NBUF) * a.buf_stride);
   };
-  auto rows_in = [&](unsigned b) -> unsigned { return min(B, nrows - b * B); };
+  auto rows_at = [&](unsigned long long row) -> unsigned {
+    return static_cast<unsigned>(min(static_cast<unsigned long long>(B), a.rows - row));
+  };
   TR_DECL
 
   if (warp == NW) {
@@ -492,11 +602,56 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     // is done and refills the slot once the bulk engine has read it.
     if (lane != 0) return;
     const uint64_t pol = a.evict_first ? policy_evict_first() : policy_evict_normal();
+    const unsigned long long nbt = (a.rows + B - 1) / B;  // batches of the whole matrix
+    const unsigned long long mtag = static_cast<unsigned long long>(ctl->sweep_seq) << 32;
+    ulonglong2* mail = a.mail + static_cast<size_t>(group) * kMail;
+    unsigned nb = 0xffffffffu;  // local batches with rows (known at the first sentinel)
+    // first row of local batch b, or kNoRow
+    auto pick = [&](unsigned b) -> unsigned long long {
+      if (b >= nb) return kNoRow;
+      unsigned long long row;
+      // (the seed sweep has no row exchange to bound how far a leader runs
+      // ahead of its followers, so with G > 1 it keeps the static blocks)
+      if (!a.dyn || (SEED && G > 1)) {
+        row = b < nb_static ? r0 + static_cast<unsigned long long>(b) * B : kNoRow;
+      } else if (G == 1 || g == 0) {
+        const unsigned long long t = atomicAdd(&ctl->batch_next, 1ull);
+        row = t < nbt ? t * B : kNoRow;
+        if (G > 1) st_relaxed_b128(&mail[b % kMail], row, mtag | (b + 1));
+      } else {
+        unsigned long long lo, hi;
+        ld_relaxed_b128(&mail[b % kMail], lo, hi);
+        if (hi != (mtag | (b + 1))) {
+          const unsigned long long t0 = globaltimer_ns();
+          unsigned n = 0;
+          do {
+            ld_relaxed_b128(&mail[b % kMail], lo, hi);
+            if (hi != (mtag | (b + 1)) && (++n & 255u) == 0 && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
+#ifdef UOT_DEBUG
+              printf("mail timeout cta %u group %u b %u want %llx seen %llx\n", cta, group, b, mtag | (b + 1), hi);
+#endif
+              atomicOr(&ctl->status, kStatusExchangeTimeout);
+              lo = kNoRow;
+              break;
+            }
+          } while (hi != (mtag | (b + 1)));
+        }
+        row = lo;
+      }
+      if (row == kNoRow) nb = b;
+      return row;
+    };
     auto issue_load = [&](unsigned b) {
-      const unsigned nr = rows_in(b);
+      const unsigned long long row = pick(b);
       uint64_t* bar = &full[b % NBUF];
+      srow[b % NBUF] = row;
+      if (row == kNoRow) {  // sentinel: the consumers stop here
+        mbar_arrive(bar);
+        return;
+      }
+      const unsigned nr = rows_at(row);
       T* dst = slot_ptr(b);
-      const T* src = gbase + static_cast<size_t>(b) * B * a.pitch;
+      const T* src = gbase + row * a.pitch;
       mbar_arrive_expect_tx(bar, nr * row_bytes);
       if (G == 1) {
         bulk_g2s(dst, src, nr * row_bytes, bar, pol);  // rows contiguous when G == 1
@@ -506,9 +661,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       }
     };
     auto issue_store = [&](unsigned b) {
-      const unsigned nr = rows_in(b);
+      const unsigned long long row = srow[b % NBUF];
+      const unsigned nr = rows_at(row);
       const T* srcs = slot_ptr(b);
-      T* dst = gbase + static_cast<size_t>(b) * B * a.pitch;
+      T* dst = gbase + row * a.pitch;
       if (G == 1) {
         bulk_s2g(dst, srcs, nr * row_bytes, pol);
       } else {
@@ -520,18 +676,20 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
 #ifdef UOT_TRACE
     const unsigned long long tr_p0 = clock64();
 #endif
-    for (unsigned b = 0; b < nb && b < static_cast<unsigned>(NBUF); ++b) issue_load(b);
+    // Sentinels go to local batches nb .. nb+NF-1: the compute warps stop at
+    // nb, factor warp f at its first batch >= nb.
+    for (unsigned b = 0; b < static_cast<unsigned>(NBUF); ++b) issue_load(b);
     for (unsigned b = 0; b < nb; ++b) {
       TR_BEGIN();
       mbar_wait(&done2[b % NBUF], (b / NBUF) & 1u);  // slot b consumed (sweep 2 / seed done)
       TR_END(4);
       if (SEED) {
-        if (b + NBUF < nb) issue_load(b + NBUF);
+        if (b + NBUF - NF < nb) issue_load(b + NBUF);
         continue;
       }
       issue_store(b);
       // refill the slot of the previous batch: its store has had a whole batch to drain
-      if (b >= 1 && b - 1 + NBUF < nb) {
+      if (b >= 1 && b - 1 + NBUF - NF < nb) {
         bulk_wait_read<1>();
         issue_load(b - 1 + NBUF);
       }
@@ -557,11 +715,15 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
 #ifdef UOT_TRACE
     const unsigned long long tr_f0 = clock64();
 #endif
-    for (unsigned s = f; s < nb; s += NF) {
-      const unsigned nr = rows_in(s);
+    for (unsigned s = f;; s += NF) {
+      // the slot's first row (the slot cannot be refilled before this warp's alpha)
+      mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
+      const unsigned long long row = srow[s % NBUF];
+      if (row == kNoRow) break;
+      const unsigned nr = rows_at(row);
       const unsigned q = s % kQ;
       double rv = 0.0;
-      if (lane < static_cast<int>(nr)) rv = __ldg(&a.rpd[r0 + static_cast<unsigned long long>(s) * B + lane]);
+      if (lane < static_cast<int>(nr)) rv = __ldg(&a.rpd[row + lane]);
       TR_BEGIN();
       mbar_wait(&done1[q], (s / kQ) & 1u);
       TR_END(0);
@@ -579,13 +741,18 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       TR_BEGIN();
       if (lane < static_cast<int>(nr)) {
         double al;
+#if UOT_EXP
+        al = 1.0;  // experiment builds: the row sums are not computed
+        if (false) {
+#else
         if (!rescale_factor_dev(rv, t, a.fi, &al)) {
+#endif
           atomicOr(&ctl->alpha_bad, 1);
           al = 1.0;
         }
         alpha_s[q * BM + lane] = al;
         if (g == 0) {
-          a.alpha[r0 + static_cast<unsigned long long>(s) * B + lane] = al;
+          a.alpha[row + lane] = al;
           errmax = fmax(errmax, fabs(al - 1.0));
         }
       }
@@ -611,7 +778,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   // ========================================================= compute warps ==
   double beta[EPC * V], acc[EPC * V];
 #pragma unroll
-  for (int i = 0; i < EPC * V; ++i) acc[i] = 0.0;
+  for (int i = 0; i < EPC * V; ++i) acc[i] = UOT_EXP ? 1.0 : 0.0;  // (experiments: positive column sums)
   ScreenBounds sb{0xffffffffu, 0u};
   if (!SEED) {
     const double* bsrc = a.beta2 + ((ctl->iter + 1) & 1ull) * a.pitch + static_cast<size_t>(g) * a.slice;
@@ -623,15 +790,23 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     }
     if (!F64) sb = screen_bounds(beta, EPC * V);
   }
+  // this thread's TMEM factor columns (TB): lane quarter warp%4, column block warp/4
+  const uint32_t tcol = tbase + (static_cast<uint32_t>(32 * (warp % 4)) << 16) + 8 * V * (warp / 4);
+  if (TB) {
+#pragma unroll
+    for (int k = 0; k < V; ++k) tmem_st_chunk(tcol + 8 * k, beta + 4 * k);
+    tmem_wait_st_();
+  }
 
 #ifdef UOT_TRACE
   const unsigned long long tr_c0 = clock64();
 #endif
   if (SEED) {
-    for (unsigned s = 0; s < nb; ++s) {
+    for (unsigned s = 0;; ++s) {
       mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
+      if (srow[s % NBUF] == kNoRow) break;
       const T* buf = slot_ptr(s);
-      const unsigned nr = rows_in(s);
+      const unsigned nr = rows_at(srow[s % NBUF]);
 #pragma unroll
       for (int r = 0; r < BM; ++r)
         if (r < static_cast<int>(nr)) {
@@ -644,20 +819,32 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       if (lane == 0) mbar_arrive(&done2[s % NBUF]);
     }
   } else {
-    uint64_t x1bad = 0;  // bit (b % 8) * 8 + r: row r of batch b took the exact path in sweep 1
-    for (unsigned s = 0; s < nb + LA + 1; ++s) {
-      const bool s1 = s < nb;                                                    // sweep 1 of batch s
+    // bit (b % 8) * BM + r: row r of batch b took the exact path in sweep 1
+    using Mask = typename std::conditional<(BM <= 4), uint32_t, uint64_t>::type;
+    Mask x1bad = 0;
+    unsigned nb = 0xffffffffu;        // local batches (set at the sentinel)
+    unsigned slot1 = 0, ph1 = 0;      // ring slot and full-barrier parity of batch s
+    unsigned slot2 = 0;               // ring slot of batch b = s - LA - 1
+    for (unsigned s = 0;; ++s) {
+      bool s1 = s < nb;  // sweep 1 of batch s
+      if (s1) {
+        TR_BEGIN();
+        mbar_wait(&full[slot1], ph1);
+        TR_END(16);
+        if (srow[slot1] == kNoRow) {
+          nb = s;
+          s1 = false;
+        }
+      }
       const bool s2 = s >= static_cast<unsigned>(LA + 1) && s - (LA + 1) < nb;  // sweep 2 of batch b
+      if (!s1 && s >= nb + LA + 1) break;  // (nb is known once s1 is false)
       const unsigned b = s - (LA + 1);
       double part[BM];
       if (s1) {
-        TR_BEGIN();
-        mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
-        TR_END(16);
-        T* buf = slot_ptr(s);
-        const unsigned nr = rows_in(s);
-        const unsigned sh = (s % 8) * 8;
-        x1bad &= ~(0xffull << sh);
+        T* buf = reinterpret_cast<T*>(smem + slot1 * a.buf_stride);
+        const unsigned nr = BM == 1 ? 1u : rows_at(srow[slot1]);
+        const unsigned sh = (s % 8) * BM;
+        x1bad &= ~(static_cast<Mask>((1u << BM) - 1u) << sh);
 #pragma unroll
         for (int r = 0; r < BM; ++r) {
           part[r] = 0.0;
@@ -665,10 +852,18 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
             if constexpr (F64) {
               part[r] = row_sweep1_f64<NT, V, FULL>(reinterpret_cast<double2*>(buf + r * a.slice), tid, nq, beta);
             } else {
+#if UOT_EXP
+              exp_touch<NT, V>(reinterpret_cast<float4*>(buf + r * a.slice), tid);
+#else
               bool bad = false;
-              part[r] =
-                  row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, sb, bad);
-              if (bad) x1bad |= 1ull << (sh + r);
+              if constexpr (TB)
+                part[r] = row_sweep1_tb<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, tcol,
+                                                     sb, bad);
+              else
+                part[r] =
+                    row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, sb, bad);
+              if (bad) x1bad |= static_cast<Mask>(1u) << (sh + r);
+#endif
             }
           }
         }
@@ -677,9 +872,9 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         TR_BEGIN();
         mbar_wait(&alpha_rdy[b % kQ], (b / kQ) & 1u);
         TR_END(19);
-        T* buf = slot_ptr(b);
-        const unsigned nr = rows_in(b);
-        const unsigned sh = (b % 8) * 8;
+        T* buf = reinterpret_cast<T*>(smem + slot2 * a.buf_stride);
+        const unsigned nr = BM == 1 ? 1u : rows_at(srow[slot2]);
+        const unsigned sh = (b % 8) * BM;
 #pragma unroll
         for (int r = 0; r < BM; ++r)
           if (r < static_cast<int>(nr)) {
@@ -687,16 +882,21 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
               row_sweep2_f64<NT, V, FULL>(reinterpret_cast<double2*>(buf + r * a.slice), tid, nq,
                                           alpha_s[(b % kQ) * BM + r], acc);
             else
+#if UOT_EXP
+              exp_touch<NT, V>(reinterpret_cast<float4*>(buf + r * a.slice), tid);
+#else
               row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq,
-                                      alpha_s[(b % kQ) * BM + r], (x1bad >> (sh + r)) & 1ull, acc);
+                                      alpha_s[(b % kQ) * BM + r], (x1bad >> (sh + r)) & 1u, acc);
+#endif
           }
         fence_proxy_async_smem();  // generic writes -> the producer's bulk store
         __syncwarp();
-        if (lane == 0) mbar_arrive(&done2[b % NBUF]);
+        if (lane == 0) mbar_arrive(&done2[slot2]);
+        slot2 = slot2 + 1 == NBUF ? 0 : slot2 + 1;
       }
       if (s1) {  // row partials of batch s (after sweep 2, whose work hides the shuffle latency)
         const unsigned qq = s % kQ;
-        const unsigned nr = rows_in(s);
+        const unsigned nr = BM == 1 ? 1u : rows_at(srow[slot1]);
 #pragma unroll
         for (int r = 0; r < BM; ++r) {
           if (r < static_cast<int>(nr)) {
@@ -707,6 +907,18 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         __syncwarp();
         if (lane == 0) mbar_arrive(&done1[qq]);
       }
+      if (++slot1 == NBUF) {
+        slot1 = 0;
+        ph1 ^= 1u;
+      }
+    }
+  }
+  if (TB) {  // every compute warp is done with TMEM: compute warp 0 frees it
+    tmem_fence_before_();
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    if (warp == 0) {
+      tmem_fence_after_();
+      tmem_dealloc_cols<kTbCols>(tbase);
     }
   }
 #ifdef UOT_TRACE

@@ -79,6 +79,12 @@ struct SweepCfg {
 #ifndef UOT_TM_S2FIRST
 #define UOT_TM_S2FIRST 1
 #endif
+// Column factors of sweep 1 parked in TMEM (sweep.cuh, TB) for slices of 3-4
+// float4 per thread: frees the registers that otherwise spill (measured +5-8%
+// at 32768^2 .. 16384^2; at V = 2 the factors fit registers and TMEM loses).
+#ifndef UOT_TMEM_BETA
+#define UOT_TMEM_BETA 1
+#endif
 template <int NT, int V, int BM, int NB, bool XCHG = false>
 SweepCfg make_cfg() {
   constexpr int LA = XCHG ? UOT_LA_X : UOT_LA_G1;
@@ -93,8 +99,9 @@ SweepCfg make_cfg() {
   c.nbuf = NB;
   c.nf = NF;
   c.xchg = XCHG;
-  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false>;
-  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false>;
+  constexpr bool TB = UOT_TMEM_BETA && V >= 3;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false, float, TB>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false, float, TB>;
   c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true>;
   c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
@@ -258,6 +265,8 @@ struct uot_ctx {
   int evict_first = 0;
   int full = 0;
   int smid_map = 0;
+  int dyn = 1;  // batches handed out by a global counter (SweepArgs::dyn)
+  ulonglong2* mail = nullptr;  // [groups][kMail] batch picks of the group leaders
   size_t smem_tm = 0;    // dynamic smem of the TMEM-lag iteration kernel
   // resident mode: the whole uot_iterate call is one persistent launch
   const ResidentCfg* rcfg = nullptr;
@@ -378,6 +387,7 @@ int plan_layout(uot_ctx* ctx) {
   int smem_optin = 0;
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   // the TMEM-lag kernel's rings + factor rings must fit next to each other
+  ctx->dyn = env_int("UOT_DYNAMIC", 1) != 0;
   ctx->use_tmem = !f64 && env_int("UOT_TMEM", 0) != 0 && ctx->smem_tm <= static_cast<size_t>(smem_optin);
   ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * ctx->esz > (64ull << 20) ? 1 : 0;
   ctx->full = slice == epc * cfg->nt * cfg->v ? 1 : 0;
@@ -449,6 +459,9 @@ int alloc_all(uot_ctx* ctx) {
   if ((rc = dalloc(ctx, &ctx->cta_err, kErrSlots * static_cast<size_t>(ctx->grid)))) return rc;
   const size_t xn = static_cast<size_t>(ctx->grid) * kRing;
   if ((rc = dalloc(ctx, &ctx->xrec, xn))) return rc;
+  const size_t mn = static_cast<size_t>(ctx->grid) * kMail;  // >= groups * kMail
+  if ((rc = dalloc(ctx, &ctx->mail, mn))) return rc;
+  CK(cudaMemsetAsync(ctx->mail, 0, mn * sizeof(ulonglong2), ctx->stream));
   if ((rc = dalloc(ctx, &ctx->ctl, 1))) return rc;
   if ((rc = dalloc(ctx, &ctx->dflag, 1))) return rc;
   if ((rc = dalloc(ctx, &ctx->bar_flags, std::max<size_t>(ctx->grid, ctx->sms)))) return rc;
@@ -495,6 +508,8 @@ SweepArgs sweep_args(const uot_ctx* ctx) {
   a.buf_stride = ctx->buf_stride;
   a.evict_first = ctx->evict_first;
   a.smid_map = ctx->smid_map;
+  a.dyn = ctx->dyn;
+  a.mail = ctx->mail;
   a.fi = ctx->fi;
   return a;
 }
@@ -905,6 +920,12 @@ int uot_peer_connect(uot_ctx* ctx, const uint8_t* handles) {
 
 int uot_exchange_mode(const uot_ctx* ctx) { return ctx ? ctx->xmode : -1; }
 
+int uot_set_deterministic(uot_ctx* ctx, int on) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  ctx->dyn = on ? 0 : 1;
+  return UOT_OK;
+}
+
 int uot_set_variant(uot_ctx* ctx, int variant) {
   if (!ctx) return UOT_INVALID_PARAMETER;
   if (variant != UOT_VARIANT_FUSED && variant != UOT_VARIANT_TWO_PASS && variant != UOT_VARIANT_BASELINE)
@@ -942,7 +963,7 @@ void uot_destroy(uot_ctx* ctx) {
   if (ctx->d_peers) cudaFree(ctx->d_peers);
   for (auto e : ctx->ev) cudaEventDestroy(e);
   void* bufs[] = {ctx->P,     ctx->rpd,   ctx->cpd,      ctx->alpha,   ctx->beta2, ctx->col_sums, ctx->xsum,
-                  ctx->partials, ctx->cta_err, ctx->xrec, ctx->ctl, ctx->dflag, ctx->bar_flags,
+                  ctx->partials, ctx->cta_err, ctx->xrec, ctx->mail, ctx->ctl, ctx->dflag, ctx->bar_flags,
                   ctx->abl_partials, ctx->abl_row_err};
   for (void* p : bufs)
     if (p) cudaFree(p);
@@ -971,6 +992,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->resident = ctx->rcfg ? 1 : 0;
   o->persist = ctx->use_persist ? 1 : 0;
   o->dtype = ctx->dtype;
+  o->dynamic = ctx->dyn;
   o->nbuf = ctx->cfg->nbuf;
   o->sms = ctx->sms;
   o->rank = ctx->rank;

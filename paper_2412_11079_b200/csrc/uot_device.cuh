@@ -39,6 +39,8 @@ struct Control {
   unsigned int pad_;
   double rerr_beta[3];        // resident kernel: max|beta(t)-1| at slot t%3
   double rerr_alpha[3];       // resident kernel: max|alpha(t)-1| at slot t%3
+  unsigned long long batch_next;  // dynamic sweep: next batch to hand out (0 between sweeps)
+  unsigned long long sweep_seq;   // never reset: completed sweep + finalize pairs (mail tags)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

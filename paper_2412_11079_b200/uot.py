@@ -88,7 +88,8 @@ class Layout(C.Structure):
                 ("nbuf", C.c_uint32), ("sms", C.c_uint32), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("device", C.c_int32), ("evict_first", C.c_int32),
                 ("smid_map", C.c_int32), ("exchange", C.c_int32), ("tmem", C.c_int32),
-                ("resident", C.c_int32), ("persist", C.c_int32), ("dtype", C.c_int32)]
+                ("resident", C.c_int32), ("persist", C.c_int32), ("dtype", C.c_int32),
+                ("dynamic", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -122,6 +123,7 @@ def lib():
     L.uot_peer_connect.argtypes = [_P, _P]
     L.uot_exchange_mode.argtypes = [_P]
     L.uot_set_variant.argtypes = [_P, _i]
+    L.uot_set_deterministic.argtypes = [_P, _i]
     L.uot_problem_file_info.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_i),
                                         C.POINTER(_d), C.POINTER(_d)]
     L.uot_last_io_error.restype = C.c_char_p
@@ -525,6 +527,12 @@ class Session:
         if name not in self.VARIANTS:
             _raise(1, f"unknown iteration variant {name!r}")
         self._check(lib().uot_set_variant(self._h, self.VARIANTS[name]))
+
+    def set_deterministic(self, on: bool = True):
+        """Fixed row blocks per CTA group (bit-reproducible run to run) instead
+        of the default dynamic batch schedule (uot_set_deterministic)."""
+        self._check(lib().uot_set_deterministic(self._h, 1 if on else 0))
+        self.layout["dynamic"] = 0 if on else 1
 
     def set_timing(self, on: bool = True):
         self._check(lib().uot_set_timing(self._h, 1 if on else 0))

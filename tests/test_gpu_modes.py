@@ -130,3 +130,26 @@ def test_persistent_streaming_early_exit(gpu, orc):
     r = run(gpu, a, rpd, cpd, 1.0, 0.0, 10000, tol=1e-6, env={"UOT_PERSIST": "1", "UOT_RESIDENT": "0"})
     assert r[6]["persist"] == 1 and ref.converged and r[5] and r[3] == ref.iterations
     assert_parity(r[0], ref.plan, rpd, cpd, "persist converged")
+
+
+@pytest.mark.parametrize("m,n,k", [(3000, 32768, 4), (20000, 4096, 5), (4099, 8192, 4)])
+def test_batch_schedules(gpu, orc, m, n, k):
+    """Dynamic batches (default: a device counter hands out row batches) and the
+    deterministic schedule (fixed row blocks, uot_set_deterministic) both meet the
+    parity bar; the deterministic one reproduces itself bit for bit."""
+    a, rpd, cpd = orc.gen_problem(11, m, n)
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 4)
+    out = {}
+    for name, det in (("det1", True), ("det2", True), ("dyn", False)):
+        with gpu.Session(m, n) as s:
+            s.set_deterministic(det)
+            assert s.layout["dynamic"] == (0 if det else 1)
+            s.set_problem(gpu.Problem(a, rpd, cpd, 1.0, 0.1))
+            s.init_col_sums()
+            it, err, conv = s.iterate(k, KNEVER)
+            assert it == k
+            out[name] = (s.plan(), s.factors())
+        assert_parity(out[name][0], ref.plan, rpd, cpd, f"{m}x{n} {name}")
+        np.testing.assert_allclose(out[name][1].alpha, ref.alpha, rtol=1e-10)
+    assert np.array_equal(out["det1"][0], out["det2"][0])
+    np.testing.assert_array_equal(out["det1"][1].alpha, out["det2"][1].alpha)

@@ -95,11 +95,14 @@ def test_golden_big_anchors(gpu, big_golden):
         rows = data[key + "_rows"]
         ref_rows = data[key + "_plan_rows"]
         assert np.max(np.abs(plan[rows].astype(np.float64) - ref_rows) / ref_rows) <= TOL, key
+        # factors and column sums: f64 sums over ~10^4-10^5 terms whose order
+        # follows the dynamic batch schedule (which CTA took which rows), so
+        # they agree to a few 1e-12 rather than bit for bit
         st = int(data[key + "_alpha_stride"][0])
-        np.testing.assert_allclose(f.alpha[::st], data[key + "_alpha_strided"], rtol=1e-12, err_msg=key)
+        np.testing.assert_allclose(f.alpha[::st], data[key + "_alpha_strided"], rtol=1e-10, err_msg=key)
         cst = int(data[key + "_col_stride"][0])
-        np.testing.assert_allclose(f.beta[::cst], data[key + "_beta_strided"], rtol=1e-12, err_msg=key)
-        np.testing.assert_allclose(cs[::cst], data[key + "_colsums_strided"], rtol=1e-12, err_msg=key)
+        np.testing.assert_allclose(f.beta[::cst], data[key + "_beta_strided"], rtol=1e-10, err_msg=key)
+        np.testing.assert_allclose(cs[::cst], data[key + "_colsums_strided"], rtol=1e-10, err_msg=key)
         total = plan.astype(np.float64).sum()
         assert abs(total - data[key + "_sum"][0]) <= 1e-9 * data[key + "_sum"][0], key
         assert abs(err - data[key + "_err"][0]) <= TOL * data[key + "_err"][0], key
