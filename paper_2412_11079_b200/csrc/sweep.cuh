@@ -591,9 +591,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   auto slot_ptr = [&](unsigned b) -> T* {
     return reinterpret_cast<T*>(smem + (b % NBUF) * a.buf_stride);
   };
-  auto rows_at = [&](unsigned long long row) -> unsigned {
-    return static_cast<unsigned>(min(static_cast<unsigned long long>(B), a.rows - row));
-  };
+  // A slot's batch travels as {first row, rows} packed into 64 bits (rows in
+  // the top byte): static blocks end inside a batch, dynamic batches at `rows`.
+  auto rows_at = [](unsigned long long v) -> unsigned { return static_cast<unsigned>(v >> 56); };
+  auto row_of = [](unsigned long long v) -> unsigned long long { return v & ((1ull << 56) - 1); };
   TR_DECL
 
   if (warp == NW) {
@@ -613,10 +614,13 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       // (the seed sweep has no row exchange to bound how far a leader runs
       // ahead of its followers, so with G > 1 it keeps the static blocks)
       if (!a.dyn || (SEED && G > 1)) {
+        const unsigned long long end = r0 + base + (group < rem ? 1 : 0);
         row = b < nb_static ? r0 + static_cast<unsigned long long>(b) * B : kNoRow;
+        if (row != kNoRow) row |= min(static_cast<unsigned long long>(B), end - row) << 56;
       } else if (G == 1 || g == 0) {
         const unsigned long long t = atomicAdd(&ctl->batch_next, 1ull);
         row = t < nbt ? t * B : kNoRow;
+        if (row != kNoRow) row |= min(static_cast<unsigned long long>(B), a.rows - row) << 56;
         if (G > 1) st_relaxed_b128(&mail[b % kMail], row, mtag | (b + 1));
       } else {
         unsigned long long lo, hi;
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       }
       const unsigned nr = rows_at(row);
       T* dst = slot_ptr(b);
-      const T* src = gbase + row * a.pitch;
+      const T* src = gbase + row_of(row) * a.pitch;
       mbar_arrive_expect_tx(bar, nr * row_bytes);
       if (G == 1) {
         bulk_g2s(dst, src, nr * row_bytes, bar, pol);  // rows contiguous when G == 1
@@ -664,7 +668,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       const unsigned long long row = srow[b % NBUF];
       const unsigned nr = rows_at(row);
       const T* srcs = slot_ptr(b);
-      T* dst = gbase + row * a.pitch;
+      T* dst = gbase + row_of(row) * a.pitch;
       if (G == 1) {
         bulk_s2g(dst, srcs, nr * row_bytes, pol);
       } else {
@@ -718,9 +722,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     for (unsigned s = f;; s += NF) {
       // the slot's first row (the slot cannot be refilled before this warp's alpha)
       mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
-      const unsigned long long row = srow[s % NBUF];
-      if (row == kNoRow) break;
-      const unsigned nr = rows_at(row);
+      const unsigned long long packed = srow[s % NBUF];
+      if (packed == kNoRow) break;
+      const unsigned nr = rows_at(packed);
+      const unsigned long long row = row_of(packed);
       const unsigned q = s % kQ;
       double rv = 0.0;
       if (lane < static_cast<int>(nr)) rv = __ldg(&a.rpd[row + lane]);
