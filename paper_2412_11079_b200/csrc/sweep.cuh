@@ -157,8 +157,8 @@ __device__ __forceinline__ double exchange_row_sum(ulonglong2* xrec, unsigned ct
 // values is screened with one VIADDMNMX per value against a per-thread window
 // (ScreenBounds) that certifies x0 AND x1 = f32(f64(x0)*beta_j) positive normal;
 // otherwise the group takes exact hardware conversions. The column sums widen
-// x2 with the exact hardware conversion (no screen: the next iteration screens
-// x2 as its x0). f64 -> f32 is one F2F.F32.F64 (RN), the reference's T(double).
+// x2 with fastd after a screen of the group's x2 (nn_max), else the hardware
+// conversion. f64 -> f32 is one F2F.F32.F64 (RN), the reference's T(double).
 
 __device__ __forceinline__ uint32_t nn_max(uint32_t m, float x) {
   return max(m, __float_as_uint(x) - 0x800000u);  // >= 0x7f000000 <=> not positive normal
@@ -256,6 +256,12 @@ __device__ __forceinline__ void group_sweep1(float4* row, float4 (&v)[KG], uint3
 
 // Sweep 2 of one chunk group (fused.hpp:135-142): x <- f32(f64(x)*alpha) in
 // place, next_j += f64(x). EXACT: x1 may be non-normal (hardware widening).
+// UOT_S2_FASTD: the column sums widen x2 with fastd after a screen of the
+// group (off the 16/clk/SM conversion pipe): +1.3% at 32768^2 (measured);
+// 0 = the hardware conversion for every value.
+#ifndef UOT_S2_FASTD
+#define UOT_S2_FASTD 1
+#endif
 template <int NT, int KG, bool FULL, bool EXACT>
 __device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g0, unsigned tid, unsigned nq,
                                              double al, double* acc) {
@@ -264,13 +270,32 @@ __device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       comp(w[kk], e) = d2f((EXACT ? static_cast<double>(comp(w[kk], e)) : fastd(comp(w[kk], e))) * al);
+#if UOT_S2_FASTD
+  // x2 screened positive normal: widen with integer ops (off the conversion pipe)
+  uint32_t m = 0;
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m = nn_max(m, comp(w[kk], e));
+  const bool ok = nn_ok(m);
+#endif
 #pragma unroll
   for (int kk = 0; kk < KG; ++kk) {
     const unsigned q = tid + (g0 + kk) * NT;
     if (FULL || q < nq) {
       row[q] = w[kk];
+#if UOT_S2_FASTD
+      if (ok) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += fastd(comp(w[kk], e));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(w[kk], e));
+      }
+#else
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(w[kk], e));
+#endif
     }
   }
 }
@@ -875,7 +900,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       }
       if (s2) {  // sweep 2 of batch s-1-LA once its factors are published
         TR_BEGIN();
-        mbar_wait(&alpha_rdy[b % kQ], (b / kQ) & 1u);
+        mbar_wait(&alpha_rdy[b % kQ], (b / kQ) & 1u);  // (plain / nanosleep polls: measured no faster)
         TR_END(19);
         T* buf = reinterpret_cast<T*>(smem + slot2 * a.buf_stride);
         const unsigned nr = BM == 1 ? 1u : rows_at(srow[slot2]);
