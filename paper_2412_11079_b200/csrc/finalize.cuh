@@ -110,9 +110,21 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
 
   double s = 0.0;  // column sum of column j (valid in warp 0)
   if (REDUCE) {
+    // Same ascending-k order of additions as a plain loop, with the L2 loads of
+    // 8 rows issued together (a serial loop paid one L2 round trip per row:
+    // 13 us at 148 groups).
     double p = 0.0;
-    if (j < f.cols)
-      for (unsigned k = slice; k < f.groups; k += kFinSlices) p += f.partials[static_cast<size_t>(k) * f.pitch + j];
+    if (j < f.cols) {
+      unsigned k = slice;
+      for (; k + 7 * kFinSlices < f.groups; k += 8 * kFinSlices) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(&f.partials[static_cast<size_t>(k + u * kFinSlices) * f.pitch + j]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p += v[u];
+      }
+      for (; k < f.groups; k += kFinSlices) p += __ldcg(&f.partials[static_cast<size_t>(k) * f.pitch + j]);
+    }
     part[slice][lane] = p;
     __syncthreads();
     if (slice == 0) {
