@@ -228,6 +228,7 @@ def run_ours(args, grp: Group):
     dev = int(os.environ.get("BENCH_DEVICE", grp.local_rank))  # BENCH_DEVICE: ranks sharing one GPU (smoke only)
 
     s = D.make_session(rows_global, COLS, dev, args.exchange)  # collective (peer handles / NCCL id)
+    exchange = s.exchange  # "nccl" when the peer mappings could not be made (make_session falls back)
     lay = s.layout
     rows_local = s.rows
 
@@ -302,7 +303,7 @@ def run_ours(args, grp: Group):
         return None
     xdesc = (", column sums exchanged once per iteration inside the finalize kernels over peer memory "
              "(CUDA IPC, NVLink): cols+1 f64 pushed to every rank, ascending-rank sum") \
-        if args.exchange == "peer" else ", NCCL allreduce of cols+N f64 per iteration"
+        if exchange == "peer" else ", NCCL allreduce of cols+N f64 per iteration"
     return {
         "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,

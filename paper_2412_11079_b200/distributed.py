@@ -25,6 +25,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import time
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -139,17 +140,42 @@ def make_session(global_rows: int, cols: int, device: int | None = None,
     if device is None:
         device = int(os.environ.get("LOCAL_RANK", rank))
     exchange = exchange or os.environ.get("UOT_EXCHANGE", "peer")
+    if world > 1 and exchange == "peer":
+        s = DistSession(global_rows, cols, rank, world, device, None, "peer")
+        why = _connect_peers(s)
+        if why is None:
+            return s
+        s.close()
+        # Every rank saw the same verdict (all-gathered), so all fall back together.
+        if os.environ.get("UOT_EXCHANGE_FALLBACK", "1") == "0":
+            raise uot.CudaError(f"peer exchange unavailable: {why}")
+        warnings.warn(f"peer exchange unavailable ({why}); using one NCCL allreduce per iteration")
+        exchange = "nccl"
     nid = None
     if world > 1 and exchange == "nccl":
         nid = broadcast_bytes(nccl_unique_id() if rank == 0 else None, src=0)
-    s = DistSession(global_rows, cols, rank, world, device, nid, exchange)
-    if world > 1 and exchange == "peer":
+    return DistSession(global_rows, cols, rank, world, device, nid, exchange)
+
+
+def _connect_peers(s: DistSession) -> str | None:
+    """Collective: exchange the IPC handles and map every peer's region. Returns
+    None when every rank connected, else the first failure (same on all ranks)."""
+    try:
+        h = s.handle()
+    except uot.Error as e:
+        h = b"!" + str(e).encode()[:200]
+    handles = all_gather_bytes(h)
+    bad = [x for x in handles if len(x) != 64]
+    err = b""
+    if bad:
+        err = bad[0][1:]
+    else:
         try:
-            s.connect(all_gather_bytes(s.handle()))
-        except BaseException:
-            s.close()
-            raise
-    return s
+            s.connect(handles)
+        except uot.Error as e:
+            err = str(e).encode()[:200] or b"connect failed"
+    errs = [e for e in all_gather_bytes(err) if e]
+    return errs[0].decode(errors="replace") if errs else None
 
 
 def distributed_solve(p: uot.Problem, tol: float, max_iter: int, device: int | None = None,

@@ -2,7 +2,7 @@
 device-timed iterations/s and model HBM GB/s (2*R*C*4 bytes per iteration,
 metrics.cpp:69-72) next to the measured copy peak (MEASURED_PEAKS.json).
 
-python tools/configs.py [--json OUT]
+python tools/configs.py [--json OUT] [--only 2,4]
 """
 import json
 import os
@@ -22,8 +22,13 @@ try:
     peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
 except (OSError, KeyError, ValueError):
     peak = 6650.0
+only = None  # --only 2,4: a subset of the configs
+if "--only" in sys.argv:
+    only = {int(x) for x in sys.argv[sys.argv.index("--only") + 1].split(",")}
 rows = []
-for name, m, n, k in CONFIGS:
+for idx, (name, m, n, k) in enumerate(CONFIGS, 1):
+    if only and idx not in only:
+        continue
     with uot.Session(m, n) as s:
         s.generate_problem(42, 1.0, 0.1)
         s.init_col_sums()
@@ -36,5 +41,5 @@ for name, m, n, k in CONFIGS:
                  "it_per_s": it / (ms * 1e-3), "model_gbs": gbs, "frac_of_copy_peak": gbs / peak, "mode": mode})
     print(f"{name:34s} {ms * 1e3 / it:9.1f} us/iter {it / (ms * 1e-3):10.1f} it/s {gbs:7.0f} GB/s "
           f"({gbs / peak:.2f} of {peak:.0f})  [{mode}]", flush=True)
-if len(sys.argv) > 2 and sys.argv[1] == "--json":
-    json.dump({"peak_gbs": peak, "rows": rows}, open(sys.argv[2], "w"), indent=1)
+if "--json" in sys.argv:
+    json.dump({"peak_gbs": peak, "rows": rows}, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
