@@ -9,7 +9,9 @@
 //
 //   uot::fused_solve(p, tol, max_iter, workers)   ->  uot::cuda::fused_solve(p, tol, max_iter)
 //   uot::fused_iterate(a, state, p, fi)           ->  uot::cuda::fused_iterate(a, state, p, fi)
-//   uot::distributed_solve(p, tol, max_iter, P)   ->  uot::cuda::distributed_solve(p, tol, max_iter, rank, P, nccl_id)
+//   uot::distributed_solve(p, tol, max_iter, P)   ->  uot::cuda::distributed_solve(p, tol, max_iter, P)  (one process,
+//                                                     every rank on a GPU), or one process per GPU:
+//                                                     uot::cuda::distributed_solve(p, tol, max_iter, rank, P, nccl_id)
 //                                                     or uot::cuda::distributed_solve_peer(..., allgather)
 //   uot::baseline_solve(p, tol, max_iter)         ->  uot::cuda::baseline_solve(p, tol, max_iter)
 //   uot::tiled_solve(p, tol, max_iter, ...)       ->  uot::cuda::tiled_solve(p, tol, max_iter)
@@ -343,6 +345,73 @@ inline DistributedResult<float> distributed_solve_peer(const Problem<float>& p, 
   r.report.wall_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return r;
+}
+
+// distributed_solve(p, tol, max_iter, RankPartition | ranks) (distributed.hpp:52-142)
+// with the reference's own signature: every rank in THIS process
+// (uot_create_group), rank r on GPU r mod (visible GPUs), one fused peer-memory
+// exchange of the column sums per iteration; the whole plan and alpha come back,
+// as in the reference. Blocks must be contiguous and non-empty.
+inline DistributedResult<float> distributed_solve(const Problem<float>& p, double tol, std::size_t max_iter,
+                                                  const RankPartition& part) {
+  require_valid(p);
+  if (!(tol > 0.0)) throw InvalidParameter("distributed_solve: tol must be positive");
+  if (max_iter < 1) throw InvalidParameter("distributed_solve: max_iter must be at least 1");
+  const std::size_t m = p.m(), n = p.n(), R = part.ranks;
+  if (part.blocks.size() != R || part.blocks.empty() || part.blocks.back().end != m)
+    throw PartitionError("distributed_solve: partition does not cover the matrix rows");
+  std::vector<std::uint64_t> bounds(R + 1, 0);
+  for (std::size_t r = 0; r < R; ++r) {
+    if (part.blocks[r].begin != bounds[r]) throw PartitionError("distributed_solve: partition blocks are not contiguous");
+    bounds[r + 1] = part.blocks[r].end;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<uot_ctx*> ctx(R, nullptr);
+  struct Guard {
+    std::vector<uot_ctx*>& c;
+    ~Guard() {
+      for (auto* x : c) uot_destroy(x);
+    }
+  } guard{ctx};
+  auto fail = [&](int rc) {
+    std::string msg = "session group";
+    for (auto* x : ctx)
+      if (x && *uot_last_error(x)) msg = uot_last_error(x);
+    raise(rc, msg);
+  };
+  int rc = uot_create_group(ctx.data(), m, n, UOT_F32, nullptr, static_cast<int>(R), bounds.data());
+  if (rc) fail(rc);
+  for (std::size_t r = 0; r < R; ++r) {
+    const std::size_t b = bounds[r];
+    if ((rc = uot_set_problem(ctx[r], p.a.row(b), p.rpd.data() + b, p.cpd.data(), p.er, p.ep))) fail(rc);
+  }
+  if ((rc = uot_group_init_col_sums(ctx.data(), static_cast<int>(R)))) fail(rc);
+  std::uint64_t it = 0;
+  double err = 0.0;
+  int conv = 0;
+  if ((rc = uot_group_iterate(ctx.data(), static_cast<int>(R), max_iter, tol, &it, &err, &conv))) fail(rc);
+  DistributedResult<float> out;
+  out.plan = Matrix<float>(m, n);
+  out.factors.alpha.resize(m);
+  out.factors.beta.resize(n);
+  for (std::size_t r = 0; r < R; ++r) {
+    const std::size_t b = bounds[r];
+    if ((rc = uot_get_plan(ctx[r], out.plan.row(b)))) fail(rc);
+    if ((rc = uot_get_factors(ctx[r], out.factors.alpha.data() + b, r == 0 ? out.factors.beta.data() : nullptr)))
+      fail(rc);
+  }
+  out.comm.allreduce_calls = it;  // one exchange of the column vector per iteration (distributed.hpp:88-94)
+  out.comm.doubles_reduced = it * n;
+  out.report.solver = "dist";
+  out.report.iterations = it;
+  out.report.final_error = err;
+  out.report.converged = conv != 0;
+  out.report.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return out;
+}
+inline DistributedResult<float> distributed_solve(const Problem<float>& p, double tol, std::size_t max_iter,
+                                                  std::size_t ranks) {
+  return distributed_solve(p, tol, max_iter, RankPartition::make(ranks, p.m()));
 }
 
 }  // namespace uot::cuda

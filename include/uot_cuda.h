@@ -107,6 +107,26 @@ UOT_API int uot_peer_connect(uot_ctx* ctx, const uint8_t* handles);
 /* 0 single GPU, 1 NCCL allreduce, 2 fused peer-memory exchange. */
 UOT_API int uot_exchange_mode(const uot_ctx* ctx);
 
+/* ---- single-process rank groups ------------------------------------------
+ * The reference's in-process distributed_solve(p, tol, max_iter, ranks |
+ * RankPartition) (distributed.hpp:52-136, 139-142): ONE process drives all
+ * ranks. uot_create_group makes `nranks` peer sessions (rank r on devices[r];
+ * devices NULL = round robin over the visible GPUs; ranks may share a GPU) over
+ * the row blocks `bounds[0..nranks]` (NULL = RankPartition::make, plan.cpp:35-44;
+ * a given partition must cover the rows with non-empty blocks, else
+ * UOT_PARTITION_ERROR) and maps their exchange regions into each other directly
+ * (peer access, no IPC). out[0..nranks) receives the sessions; on failure the
+ * caller destroys every non-null entry. Per rank: uot_set_problem with its block
+ * (uot_get_layout: row_offset, rows), then the collective calls below replace
+ * uot_init_col_sums / uot_iterate (which refuse group ranks). The exchange is the
+ * fused peer-memory one (ascending-rank sum, allreduce.cpp:6-15); stage 2 of
+ * every rank is stream-ordered after stage 1 of all ranks. */
+UOT_API int uot_create_group(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, const int* devices,
+                             int nranks, const uint64_t* bounds);
+UOT_API int uot_group_init_col_sums(uot_ctx* const* ctxs, int nranks);
+UOT_API int uot_group_iterate(uot_ctx* const* ctxs, int nranks, uint64_t k, double tol, uint64_t* iterations,
+                              double* final_error, int* converged);
+
 /* ---- problem files (.uotp, problem_io.cpp:13-141) --------------------- */
 
 /* read_problem's header checks (problem_io.cpp:106-135) without the payload:

@@ -257,6 +257,8 @@ struct uot_ctx {
   std::vector<unsigned char*> peer_ptrs;  // [nranks]; own entry = region
   unsigned char** d_peers = nullptr;      // device copy of peer_ptrs
   bool connected = false;
+  bool group_local = false;  // a rank of a single-process group (uot_create_group): direct peer pointers, no IPC
+  cudaEvent_t xev = nullptr;  // group: stage 1 of the running exchange is enqueued (cross-rank stream order)
 
   // layout
   unsigned G = 1, slice = 0, pitch = 0, groups = 1, B = 1, buf_stride = 0, grid = 1;
@@ -818,7 +820,7 @@ int uot_nccl_unique_id(uint8_t* out128) {
 namespace {
 // Rank state shared by both exchange flavours (distributed.hpp:65-79).
 int create_rank(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device, int rank,
-                int nranks) {
+                int nranks, const uint64_t* bounds = nullptr) {
   if (!out) return UOT_INVALID_PARAMETER;
   *out = nullptr;
   auto* ctx = new uot_ctx();
@@ -833,7 +835,15 @@ int create_rank(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, i
                      nranks, (unsigned long long)global_rows);
   if (rank < 0 || rank >= nranks) return ctx->fail(UOT_PARTITION_ERROR, "rank %d outside [0,%d)", rank, nranks);
   std::vector<uint64_t> b(nranks + 1);
-  balanced_bounds(nranks, global_rows, b.data());
+  if (bounds) {  // a caller's RankPartition (distributed.hpp:52-64): contiguous, covering, no empty block
+    for (int q = 0; q <= nranks; ++q) b[q] = bounds[q];
+    if (b[0] != 0 || b[nranks] != global_rows)
+      return ctx->fail(UOT_PARTITION_ERROR, "distributed_solve: partition does not cover the matrix rows");
+    for (int q = 0; q < nranks; ++q)
+      if (b[q + 1] <= b[q]) return ctx->fail(UOT_PARTITION_ERROR, "partition block %d is empty or unordered", q);
+  } else {
+    balanced_bounds(nranks, global_rows, b.data());
+  }
   ctx->global_rows = global_rows;
   ctx->row_offset = b[rank];
   ctx->rows = b[rank + 1] - b[rank];
@@ -864,9 +874,17 @@ int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtyp
   return UOT_OK;
 }
 
+int create_peer_rank(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device, int rank,
+                     int nranks, const uint64_t* bounds);
+
 int uot_create_peer(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device, int rank,
                     int nranks) {
-  int rc = create_rank(out, global_rows, cols, dtype, device, rank, nranks);
+  return create_peer_rank(out, global_rows, cols, dtype, device, rank, nranks, nullptr);
+}
+
+int create_peer_rank(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device, int rank,
+                     int nranks, const uint64_t* bounds) {
+  int rc = create_rank(out, global_rows, cols, dtype, device, rank, nranks, bounds);
   if (rc) return rc;
   uot_ctx* ctx = *out;
   if (nranks > 1) {
@@ -957,8 +975,10 @@ void uot_destroy(uot_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
   }
   if (ctx->comm) nccl().CommDestroy(ctx->comm);
-  for (int q = 0; q < static_cast<int>(ctx->peer_ptrs.size()); ++q)
-    if (q != ctx->rank && ctx->peer_ptrs[q]) cudaIpcCloseMemHandle(ctx->peer_ptrs[q]);
+  if (!ctx->group_local)
+    for (int q = 0; q < static_cast<int>(ctx->peer_ptrs.size()); ++q)
+      if (q != ctx->rank && ctx->peer_ptrs[q]) cudaIpcCloseMemHandle(ctx->peer_ptrs[q]);
+  if (ctx->xev) cudaEventDestroy(ctx->xev);
   if (ctx->region) cudaFree(ctx->region);
   if (ctx->d_peers) cudaFree(ctx->d_peers);
   for (auto e : ctx->ev) cudaEventDestroy(e);
@@ -1113,6 +1133,8 @@ int uot_set_plan_f64(uot_ctx* ctx, const double* a) {
 
 int uot_init_col_sums(uot_ctx* ctx) {
   if (!ctx) return UOT_INVALID_PARAMETER;
+  if (ctx->group_local && ctx->nranks > 1)
+    return ctx->fail(UOT_INVALID_PARAMETER, "a rank of a session group: use uot_group_init_col_sums");
   if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
   CK(cudaSetDevice(ctx->device));
   int rc = reset_state(ctx);
@@ -1167,6 +1189,8 @@ int uot_synchronize(uot_ctx* ctx) {
 int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations, double* final_error,
                       int* converged, double* device_ms) {
   if (!ctx) return UOT_INVALID_PARAMETER;
+  if (ctx->group_local && ctx->nranks > 1)
+    return ctx->fail(UOT_INVALID_PARAMETER, "a rank of a session group: use uot_group_iterate");
   if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
   if (!ctx->seeded)
     return ctx->fail(UOT_INVALID_PARAMETER, "carried column sums missing (call init_col_sums)");
@@ -1661,6 +1685,170 @@ int uot_save_problem_file(uot_ctx* ctx, const char* path) {
   CK(cudaStreamSynchronize(ctx->stream));
   if (!pwrite_all(f.fd, rpd.data(), 8 * ctx->rows, rpd_off + 8 * ctx->row_offset))
     return ctx->fail(UOT_IO_ERROR, "write_problem: short write to %s", path);
+  return UOT_OK;
+}
+
+}  // extern "C"
+
+#define CKC(c, expr)                                          \
+  do {                                                        \
+    const int _rc = (c)->cuda((expr), #expr);                 \
+    if (_rc != UOT_OK) return _rc;                            \
+  } while (0)
+
+// ---------------------------------------------- single-process rank groups --
+// The reference's distributed_solve(p, tol, max_iter, ranks | RankPartition)
+// runs every rank in ONE process (distributed.hpp:52-136). A group is that call
+// on the GPU: rank r is a peer session on devices[r] (devices may repeat), the
+// exchange regions are mapped into each other directly — one address space,
+// device pointers plus peer access, no IPC — and every collective step is
+// enqueued phase by phase: [sweep, stage 1] on every rank's stream, an event
+// per rank, then each stream waits for all ranks' events before its stage 2.
+// Stage 2 therefore never waits on a rank whose kernels are queued behind it
+// (ranks sharing a GPU cannot deadlock), and the result is the same ascending-
+// rank exchange as the multi-process path (finalize.cuh, allreduce.cpp:6-15).
+namespace {
+
+int group_check(uot_ctx* const* ctxs, int n) {
+  if (!ctxs || n < 1) return UOT_INVALID_PARAMETER;
+  for (int r = 0; r < n; ++r) {
+    uot_ctx* c = ctxs[r];
+    if (!c) return UOT_INVALID_PARAMETER;
+    if (c->nranks != n || c->rank != r || (n > 1 && !c->group_local))
+      return c->fail(UOT_INVALID_PARAMETER, "not rank %d of a %d-rank session group", r, n);
+  }
+  return UOT_OK;
+}
+
+// One collective step of every rank: [sweep,] stage 1 | events | stage 2.
+template <int MODE>
+int group_step(uot_ctx* const* c, int n, bool sweep, bool seed) {
+  int rc;
+  for (int r = 0; r < n; ++r) {
+    CKC(c[r], cudaSetDevice(c[r]->device));
+    if (sweep && (rc = launch_sweep(c[r], seed))) return rc;
+    if (n == 1) {
+      if ((rc = launch_finalize_single<MODE>(c[r]))) return rc;
+      continue;
+    }
+    finalize_kernel<MODE, true, false, kXchPeer>
+        <<<finalize_blocks(c[r]->pitch), kFinThreads, 0, c[r]->stream>>>(fin_args(c[r]));
+    c[r]->launches++;
+    CKC(c[r], cudaGetLastError());
+    CKC(c[r], cudaEventRecord(c[r]->xev, c[r]->stream));
+  }
+  if (n == 1) return UOT_OK;
+  for (int r = 0; r < n; ++r) {
+    CKC(c[r], cudaSetDevice(c[r]->device));
+    for (int q = 0; q < n; ++q)
+      if (q != r) CKC(c[r], cudaStreamWaitEvent(c[r]->stream, c[q]->xev, 0));
+    finalize_kernel<MODE, false, true, kXchPeer>
+        <<<finalize_blocks(c[r]->pitch), kFinThreads, 0, c[r]->stream>>>(fin_args(c[r]));
+    c[r]->launches++;
+    CKC(c[r], cudaGetLastError());
+  }
+  return UOT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int uot_create_group(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, const int* devices,
+                     int nranks, const uint64_t* bounds) {
+  if (!out || nranks < 1) return UOT_INVALID_PARAMETER;
+  for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    ndev = 1;  // rank 0's session reports the CUDA error
+  }
+  std::vector<int> dev(nranks);
+  for (int r = 0; r < nranks; ++r) dev[r] = devices ? devices[r] : r % ndev;
+  int rc = UOT_OK;
+  for (int r = 0; r < nranks && rc == UOT_OK; ++r) rc = create_peer_rank(&out[r], global_rows, cols, dtype, dev[r], r, nranks, bounds);
+  if (rc) return rc;  // out[r] (if set) carries the message; the caller destroys every non-null rank
+  if (nranks == 1) return UOT_OK;
+  // peer access between every pair of distinct devices (NVLink / NVSwitch)
+  for (int a = 0; a < nranks; ++a)
+    for (int b = 0; b < nranks; ++b) {
+      if (dev[a] == dev[b]) continue;
+      int can = 0;
+      CKC(out[a], cudaDeviceCanAccessPeer(&can, dev[a], dev[b]));
+      if (!can) return out[a]->fail(UOT_CUDA_ERROR, "device %d cannot access device %d (peer access)", dev[a], dev[b]);
+      CKC(out[a], cudaSetDevice(dev[a]));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(dev[b], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return out[a]->fail(UOT_CUDA_ERROR, "cudaDeviceEnablePeerAccess(%d -> %d): %s", dev[a], dev[b],
+                            cudaGetErrorString(e));
+      cudaGetLastError();  // (clear "already enabled")
+    }
+  for (int r = 0; r < nranks; ++r) {
+    uot_ctx* c = out[r];
+    CKC(c, cudaSetDevice(c->device));
+    c->peer_ptrs.assign(nranks, nullptr);
+    for (int q = 0; q < nranks; ++q) c->peer_ptrs[q] = out[q]->region;
+    CKC(c, cudaMemcpy(c->d_peers, c->peer_ptrs.data(), sizeof(unsigned char*) * nranks, cudaMemcpyHostToDevice));
+    CKC(c, cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming));
+    c->group_local = true;
+    c->connected = true;
+  }
+  return UOT_OK;
+}
+
+int uot_group_init_col_sums(uot_ctx* const* ctxs, int nranks) {
+  int rc = group_check(ctxs, nranks);
+  if (rc) return rc;
+  for (int r = 0; r < nranks; ++r) {
+    if (!ctxs[r]->have_problem) return ctxs[r]->fail(UOT_INVALID_PARAMETER, "no problem set");
+    CKC(ctxs[r], cudaSetDevice(ctxs[r]->device));
+    if ((rc = reset_state(ctxs[r]))) return rc;
+  }
+  if ((rc = group_step<kFinSeed>(ctxs, nranks, true, true))) return rc;
+  for (int r = 0; r < nranks; ++r) {
+    CKC(ctxs[r], cudaSetDevice(ctxs[r]->device));
+    if ((rc = sync_ctl(ctxs[r]))) return rc;
+    ctxs[r]->seeded = true;
+  }
+  return UOT_OK;
+}
+
+int uot_group_iterate(uot_ctx* const* ctxs, int nranks, uint64_t k, double tol, uint64_t* iterations,
+                      double* final_error, int* converged) {
+  int rc = group_check(ctxs, nranks);
+  if (rc) return rc;
+  std::vector<uint64_t> before(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    uot_ctx* c = ctxs[r];
+    if (!c->have_problem) return c->fail(UOT_INVALID_PARAMETER, "no problem set");
+    if (!c->seeded) return c->fail(UOT_INVALID_PARAMETER, "carried column sums missing (call init_col_sums)");
+    if (!(tol > 0.0)) return c->fail(UOT_INVALID_PARAMETER, "tol must be positive");
+    if (k < 1) return c->fail(UOT_INVALID_PARAMETER, "max_iter must be at least 1");
+    if (c->variant != UOT_VARIANT_FUSED) return c->fail(UOT_INVALID_PARAMETER, "groups run the fused schedule");
+    before[r] = c->h_ctl->iter;
+    CKC(c, cudaSetDevice(c->device));
+    begin_iterate_kernel<<<1, 1, 0, c->stream>>>(c->ctl, tol);
+    c->launches++;
+    CKC(c, cudaGetLastError());
+  }
+  for (uint64_t i = 0; i < k; ++i)
+    if ((rc = group_step<kFinIter>(ctxs, nranks, true, false))) return rc;
+  for (int r = 0; r < nranks; ++r) {
+    CKC(ctxs[r], cudaSetDevice(ctxs[r]->device));
+    if ((rc = sync_ctl(ctxs[r]))) return rc;
+  }
+  for (int r = 0; r < nranks; ++r)
+    if ((rc = status_of(ctxs[r]))) return rc;
+  const Control& h0 = *ctxs[0]->h_ctl;
+  for (int r = 1; r < nranks; ++r) {  // every rank derives the same factors and the same stop decision
+    const Control& h = *ctxs[r]->h_ctl;
+    if (h.iter - before[r] != h0.iter - before[0] || h.converged != h0.converged)
+      return ctxs[r]->fail(UOT_CUDA_ERROR, "rank %d stopped after %llu iterations, rank 0 after %llu", r,
+                           (unsigned long long)(h.iter - before[r]), (unsigned long long)(h0.iter - before[0]));
+  }
+  if (iterations) *iterations = h0.iter - before[0];
+  if (final_error) *final_error = h0.last_error;
+  if (converged) *converged = h0.converged;
   return UOT_OK;
 }
 

@@ -26,30 +26,14 @@ import ctypes as C
 import os
 import time
 import warnings
-from dataclasses import dataclass, field
-
-import numpy as np
 
 from . import uot
 
 
-@dataclass
-class CommStats:
-    """CommStats (distributed.hpp:24-27)."""
-    allreduce_calls: int = 0
-    doubles_reduced: int = 0
-
-
-@dataclass
-class DistributedResult:
-    """DistributedResult<T> (distributed.hpp:34-40) for THIS rank: the plan and
-    alpha of its row block, the (replicated) beta, the report and CommStats."""
-    plan: np.ndarray
-    factors: uot.ScalingFactors
-    report: uot.SolveReport
-    comm: CommStats = field(default_factory=CommStats)
-    row_begin: int = 0
-    row_end: int = 0
+# CommStats / DistributedResult (distributed.hpp:24-40) are shared with the
+# in-process uot.distributed_solve; here a result holds THIS rank's row block.
+CommStats = uot.CommStats
+DistributedResult = uot.DistributedResult
 
 
 def nccl_unique_id() -> bytes:

@@ -122,6 +122,9 @@ def lib():
     L.uot_peer_handle.argtypes = [_P, _P]
     L.uot_peer_connect.argtypes = [_P, _P]
     L.uot_exchange_mode.argtypes = [_P]
+    L.uot_create_group.argtypes = [_P, _u64, _u64, _i, _P, _i, _P]
+    L.uot_group_init_col_sums.argtypes = [_P, _i]
+    L.uot_group_iterate.argtypes = [_P, _i, _u64, _d, C.POINTER(_u64), C.POINTER(_d), C.POINTER(_i)]
     L.uot_set_variant.argtypes = [_P, _i]
     L.uot_set_deterministic.argtypes = [_P, _i]
     L.uot_problem_file_info.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_i),
@@ -226,6 +229,26 @@ class SolveResult:
 @dataclass
 class FusedState:
     col_sums: np.ndarray
+
+
+@dataclass
+class CommStats:
+    """CommStats (distributed.hpp:24-27)."""
+    allreduce_calls: int = 0
+    doubles_reduced: int = 0
+
+
+@dataclass
+class DistributedResult:
+    """DistributedResult<T> (distributed.hpp:34-40). From distributed_solve (one
+    process, every rank): the whole plan and alpha. From the per-process
+    distributed.distributed_solve: THIS rank's rows [row_begin, row_end)."""
+    plan: np.ndarray
+    factors: "ScalingFactors"
+    report: "SolveReport"
+    comm: CommStats = field(default_factory=CommStats)
+    row_begin: int = 0
+    row_end: int = 0
 
 
 @dataclass
@@ -397,6 +420,18 @@ class Session:
         self.cols = int(lay.cols)
         self.row_offset = int(lay.row_offset)
 
+    @classmethod
+    def _adopt(cls, handle, dtype) -> "Session":
+        """Wrap a session created elsewhere (uot_create_group)."""
+        self = cls.__new__(cls)
+        self._h = handle
+        self.dtype = np.dtype(dtype)
+        lay = Layout()
+        lib().uot_get_layout(self._h, C.byref(lay))
+        self.layout = lay.as_dict()
+        self.rows, self.cols, self.row_offset = int(lay.rows), int(lay.cols), int(lay.row_offset)
+        return self
+
     # -- plumbing
     def _err(self) -> str:
         return lib().uot_last_error(self._h).decode() if self._h else "session creation failed"
@@ -547,6 +582,92 @@ class Session:
 
 
 # ------------------------------------------------------------- solver API --
+
+
+class SessionGroup:
+    """Every rank of a row-sharded problem in THIS process (uot_create_group):
+    rank r is a Session over its RankPartition block on devices[r] (default:
+    round robin over the visible GPUs; ranks may share one), exchange regions
+    mapped directly between the ranks. init_col_sums / iterate are collective
+    over the ranks (uot_group_*); everything else is per rank (`ranks[r]`)."""
+
+    def __init__(self, global_rows: int, cols: int, nranks: int, devices=None, partition=None,
+                 dtype=np.float32):
+        L = lib()
+        self.dtype = np.dtype(dtype)
+        code = UOT_F64 if self.dtype == np.float64 else UOT_F32
+        n = int(nranks)
+        hs = (_P * max(n, 1))()
+        dev = None if devices is None else np.ascontiguousarray(devices, np.int32)
+        bnd = None
+        if partition is not None:
+            if partition.ranks != n or len(partition.blocks) != n:
+                _raise(3, "distributed_solve: partition does not cover the matrix rows")
+            bnd = np.array([0] + [e for _, e in partition.blocks], np.uint64)
+            if any(b != bnd[i] for i, (b, _) in enumerate(partition.blocks)):
+                _raise(3, "distributed_solve: partition blocks are not contiguous")
+        rc = L.uot_create_group(C.cast(hs, _P), int(global_rows), int(cols), code, _ptr(dev), n, _ptr(bnd))
+        self.ranks = []
+        for r in range(n):
+            if hs[r]:
+                self.ranks.append(Session._adopt(_P(hs[r]), self.dtype))
+        if rc:
+            msg = next((x._err() for x in reversed(self.ranks)), "session group creation failed")
+            self.close()
+            _raise(rc, msg)
+        self._hs = hs
+
+    def _check(self, rc: int):
+        if rc:
+            msg = "; ".join(f"rank {r}: {x._err()}" for r, x in enumerate(self.ranks) if x._err())
+            _raise(rc, msg or "session group call failed")
+
+    def init_col_sums(self):
+        self._check(lib().uot_group_init_col_sums(C.cast(self._hs, _P), len(self.ranks)))
+
+    def iterate(self, k: int = 1, tol: float = 1e-300):
+        it, err, conv = _u64(), _d(), _i()
+        self._check(lib().uot_group_iterate(C.cast(self._hs, _P), len(self.ranks), int(k), float(tol),
+                                            C.byref(it), C.byref(err), C.byref(conv)))
+        return int(it.value), float(err.value), bool(conv.value)
+
+    def close(self):
+        for x in self.ranks:
+            x.close()
+        self.ranks = []
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def distributed_solve(p: Problem, tol: float, max_iter: int, ranks=1, devices=None) -> DistributedResult:
+    """distributed_solve(p, tol, max_iter, ranks | RankPartition) (distributed.hpp:52-142)
+    in one process: every rank on a GPU (devices[r], default round robin), one
+    fused peer-memory exchange of the column sums per iteration, the whole plan
+    and alpha assembled on the host as in the reference."""
+    _validate_controls(tol, max_iter, "distributed_solve")
+    t0 = time.perf_counter()
+    part = ranks if isinstance(ranks, RankPartition) else RankPartition.make(int(ranks), p.m())
+    dt = np.float64 if np.asarray(p.a).dtype == np.float64 else np.float32
+    plan = np.empty((p.m(), p.n()), dt)
+    alpha = np.empty(p.m())
+    with SessionGroup(p.m(), p.n(), part.ranks, devices, part, dt) as g:
+        for s in g.ranks:
+            b, e = s.row_offset, s.row_offset + s.rows
+            s.set_problem(Problem(p.a[b:e], p.rpd[b:e], p.cpd, p.er, p.ep))
+        g.init_col_sums()
+        it, err, conv = g.iterate(max_iter, tol)
+        for s in g.ranks:
+            b, e = s.row_offset, s.row_offset + s.rows
+            f = s.factors()
+            alpha[b:e] = f.alpha
+            s.plan(out=plan[b:e])
+        beta = f.beta
+    rep = SolveReport("dist", it, err, conv, (time.perf_counter() - t0) * 1e3)
+    return DistributedResult(plan, ScalingFactors(alpha, beta), rep, CommStats(it, it * p.n()), 0, p.m())
 
 
 def _validate_controls(tol: float, max_iter: int, who: str):

@@ -206,6 +206,24 @@ void test_single_rank_peer_distributed() {
   CHECK(d.report.iterations == 11 && max_rel(d.plan, ref.plan) <= 1e-5);
 }
 
+void test_in_process_ranks_match_reference() {  // test_distributed.cpp:106-118, one process, reference signature
+  const auto p = random_problem(26, 301, 2000, 0.5);
+  for (std::size_t ranks : {std::size_t(2), std::size_t(3)}) {
+    const auto d = uot::cuda::distributed_solve(p, kNever, 9, ranks);
+    const auto ref = uot::distributed_solve(p, kNever, 9, ranks);
+    CHECK(d.report.iterations == 9 && d.report.solver == "dist");
+    CHECK(d.comm.allreduce_calls == ref.comm.allreduce_calls && d.comm.doubles_reduced == ref.comm.doubles_reduced);
+    CHECK(max_rel(d.plan, ref.plan) <= 1e-5);
+    CHECK(uot::max_abs_diff(d.factors.beta, ref.factors.beta) <= 1e-12);
+    CHECK(std::abs(d.report.final_error - ref.report.final_error) <= 1e-9 * std::max(1.0, ref.report.final_error));
+  }
+  uot::RankPartition gap;
+  gap.ranks = 2;
+  gap.blocks = {{0, 100}, {150, 301}};
+  CHECK_THROWS_AS(uot::cuda::distributed_solve(p, kNever, 3, gap), uot::PartitionError);
+  CHECK_THROWS_AS(uot::cuda::distributed_solve(p, kNever, 3, std::size_t(302)), uot::PartitionError);
+}
+
 }  // namespace
 
 int main() {
@@ -220,6 +238,7 @@ int main() {
       {"problem files", test_problem_files_round_trip},
       {"single-rank peer distributed", test_single_rank_peer_distributed},
       {"Problem<double>", test_f64_problem_matches_reference},
+      {"in-process ranks (reference signature)", test_in_process_ranks_match_reference},
   };
   for (const auto& [name, fn] : cases) {
     const int before = g_fail;
