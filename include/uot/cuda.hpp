@@ -8,7 +8,9 @@
 // call site by changing the namespace:
 //
 //   uot::fused_solve(p, tol, max_iter, workers)   ->  uot::cuda::fused_solve(p, tol, max_iter)
+//   uot::fused_solve(p, tol, max_iter, plan)      ->  uot::cuda::fused_solve(p, tol, max_iter, plan)
 //   uot::fused_iterate(a, state, p, fi)           ->  uot::cuda::fused_iterate(a, state, p, fi)
+//   uot::fused_iterate_parallel(a, st, p, fi, plan[, partials]) -> uot::cuda::fused_iterate_parallel(same)
 //   uot::distributed_solve(p, tol, max_iter, P)   ->  uot::cuda::distributed_solve(p, tol, max_iter, P)  (one process,
 //                                                     every rank on a GPU), or one process per GPU:
 //                                                     uot::cuda::distributed_solve(p, tol, max_iter, rank, P, nccl_id)
@@ -200,6 +202,19 @@ inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t m
   return r;
 }
 
+// fused_solve(p, tol, max_iter, const WorkerPlan&) (fused.hpp:259-285): the
+// reference's host worker plan has no GPU meaning — the sweep's CTA schedule
+// replaces it — but it is validated like the reference validates it, so a call
+// site switches by namespace alone. Results match any worker count to the
+// parity bar (the reference's own W-independence, test_fused.cpp).
+template <typename T>
+inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t max_iter, const WorkerPlan& plan,
+                                  int device = 0) {
+  if (plan.blocks.empty() || plan.blocks.back().end != p.m())
+    throw InvalidParameter("fused_solve: plan does not cover the matrix rows");
+  return fused_solve(p, tol, max_iter, device);
+}
+
 namespace detail {
 inline SolveResult<float> solve_with(const Problem<float>& p, double tol, std::size_t max_iter, int device,
                                      int variant, const char* solver, const char* who) {
@@ -272,6 +287,27 @@ inline ScalingFactors fused_iterate(Matrix<float>& a, FusedState& state, const P
   a = s.plan();
   state = s.state();
   return s.factors();
+}
+
+// fused_iterate_parallel (fused.hpp:197-257) with the reference's checks on the
+// plan and partial table; the GPU does the iteration (fused_iterate above).
+inline ScalingFactors fused_iterate_parallel(Matrix<float>& a, FusedState& state, const Problem<float>& p,
+                                             double fi, const WorkerPlan& plan, PartialTable& partials,
+                                             int device = 0) {
+  if (a.rows() != p.m() || a.cols() != p.n())
+    throw InvalidParameter("fused_iterate_parallel: matrix shape does not match problem");
+  if (state.col_sums.size() != a.cols())
+    throw InvalidParameter("fused_iterate_parallel: carried column sums have wrong length");
+  if (plan.blocks.empty() || plan.blocks.back().end != a.rows())
+    throw InvalidParameter("fused_iterate_parallel: plan does not cover the matrix rows");
+  if (partials.workers() < plan.workers || partials.cols() != a.cols())
+    throw InvalidParameter("fused_iterate_parallel: partial table does not fit the plan");
+  return fused_iterate(a, state, p, fi, device);
+}
+inline ScalingFactors fused_iterate_parallel(Matrix<float>& a, FusedState& state, const Problem<float>& p,
+                                             double fi, const WorkerPlan& plan, int device = 0) {
+  PartialTable partials(plan.workers, a.cols());
+  return fused_iterate_parallel(a, state, p, fi, plan, partials, device);
 }
 
 // distributed_solve (distributed.hpp:52-130) for rank `rank` of `nranks`

@@ -224,6 +224,29 @@ void test_in_process_ranks_match_reference() {  // test_distributed.cpp:106-118,
   CHECK_THROWS_AS(uot::cuda::distributed_solve(p, kNever, 3, std::size_t(302)), uot::PartitionError);
 }
 
+void test_worker_plan_overloads() {  // fused.hpp:197-208, 259-285: same call shapes and checks
+  const auto p = random_problem(27, 120, 500, 0.5);
+  const auto plan = uot::WorkerPlan::make(4, p.m(), p.n());
+  const auto ref = uot::fused_solve(p, kNever, 6, plan);
+  const auto gpu = uot::cuda::fused_solve(p, kNever, 6, plan);
+  CHECK(gpu.report.iterations == 6 && max_rel(gpu.plan, ref.plan) <= 1e-5);
+  uot::Matrix<float> ra = p.a, ga = p.a;
+  uot::FusedState rs{uot::init_col_sums(ra)}, gs{uot::init_col_sums(ga)};
+  const double fi = uot::compute_fi(p.er, p.ep);
+  for (int it = 0; it < 3; ++it) {
+    const auto rf = uot::fused_iterate_parallel(ra, rs, p, fi, plan);
+    const auto gf = uot::cuda::fused_iterate_parallel(ga, gs, p, fi, plan);
+    CHECK(uot::max_abs_diff(rf.beta, gf.beta) <= 1e-12);
+  }
+  CHECK(max_rel(ga, ra) <= 1e-5);
+  uot::WorkerPlan bad = plan;
+  bad.blocks.back().end -= 1;
+  CHECK_THROWS_AS(uot::cuda::fused_solve(p, kNever, 2, bad), uot::InvalidParameter);
+  CHECK_THROWS_AS(uot::cuda::fused_iterate_parallel(ga, gs, p, fi, bad), uot::InvalidParameter);
+  uot::PartialTable small(1, p.n());
+  CHECK_THROWS_AS(uot::cuda::fused_iterate_parallel(ga, gs, p, fi, plan, small), uot::InvalidParameter);
+}
+
 }  // namespace
 
 int main() {
@@ -239,6 +262,7 @@ int main() {
       {"single-rank peer distributed", test_single_rank_peer_distributed},
       {"Problem<double>", test_f64_problem_matches_reference},
       {"in-process ranks (reference signature)", test_in_process_ranks_match_reference},
+      {"WorkerPlan overloads", test_worker_plan_overloads},
   };
   for (const auto& [name, fn] : cases) {
     const int before = g_fail;
