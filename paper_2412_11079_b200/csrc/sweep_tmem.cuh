@@ -313,17 +313,24 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_tmem_kernel(const
       }
       if (XCHG) t = exchange_row_sum(a.xrec, cta, group, G, s % kRing, tag_hi | (s + 1), t, ctl);
 
+      double al = 0.0;
       if (lane < static_cast<int>(nr)) {
-        double al;
         if (!rescale_factor_dev(rv, t, a.fi, &al)) {
           atomicOr(&ctl->alpha_bad, 1);
           al = 1.0;
         }
-        alpha_s[q * BM + lane] = al;
         if (g == 0) {
           a.alpha[r0 + static_cast<unsigned long long>(s) * B + lane] = al;
           errmax = fmax(errmax, fabs(al - 1.0));
         }
+      }
+      // lane 0 — the thread that arrives on alpha_rdy — stores the batch's
+      // factors itself (release by the arriving thread: no reliance on
+      // __syncwarp cumulativity; compute-sanitizer racecheck clean)
+#pragma unroll
+      for (int r = 0; r < BM; ++r) {
+        const double v = __shfl_sync(0xffffffffu, al, r);
+        if (lane == 0 && r < static_cast<int>(nr)) alpha_s[q * BM + r] = v;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&alpha_rdy[q]);

@@ -540,7 +540,11 @@ FinalizeArgs fin_args(const uot_ctx* ctx) {
 
 int launch_sweep(uot_ctx* ctx, bool seed) {
   const SweepArgs a = sweep_args(ctx);
-  const bool xchg = !seed && ctx->G > 1;
+  // cooperative whenever G > 1: the iteration's CTAs spin on each other, and with
+  // smid_map a CTA's identity is its SM — only a co-resident grid (one CTA per
+  // SM) makes that a permutation, even for the seed sweep, when other kernels
+  // share the GPU (e.g. the ranks of a session group on one device)
+  const bool xchg = ctx->G > 1;
   const bool tm = !seed && ctx->use_tmem;
   SweepFn fn = seed ? ctx->cfg->seed[ctx->full] : (tm ? ctx->cfg->iter_tm[ctx->full] : ctx->cfg->iter[ctx->full]);
   cudaLaunchConfig_t lc{};

@@ -599,6 +599,8 @@ class SessionGroup:
         n = int(nranks)
         hs = (_P * max(n, 1))()
         dev = None if devices is None else np.ascontiguousarray(devices, np.int32)
+        if dev is not None and dev.shape != (n,):
+            _raise(1, f"SessionGroup: {dev.size} devices for {n} ranks")
         bnd = None
         if partition is not None:
             if partition.ranks != n or len(partition.blocks) != n:

@@ -31,7 +31,7 @@ def _assert_matches(res, ref, k):
 
 
 @pytest.mark.parametrize("ranks,rows,cols,k", [(2, 300, 2000, 10), (3, 257, 1000, 8), (2, 64, 20000, 6),
-                                               (4, 96, 8192, 5)])
+                                               (4, 96, 8192, 5), (2, 64, 32768, 4), (2, 100, 16384, 4)])
 def test_group_matches_distributed_solve(gpu, orc, ranks, rows, cols, k):
     uot = gpu
     a, rpd, cpd, p = _problem(uot, orc, 42, rows, cols)
@@ -91,3 +91,20 @@ def test_group_ranks_refuse_single_rank_collectives(gpu, orc):
         assert it == 3
         it, _, _ = g.iterate(2)  # resumable, like Session.iterate
         assert it == 2 and g.ranks[0].report()[0] == 5
+
+
+def test_group_f64_matches_oracle(gpu, orc):
+    uot = gpu
+    a, rpd, cpd = orc.gen_problem(11, 200, 6000, dtype=np.float64)
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, 6, 2)
+    res = uot.distributed_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KNEVER, 6, 2, devices=[0, 0])
+    assert res.plan.dtype == np.float64 and res.report.iterations == 6
+    rel = np.max(np.abs(res.plan - ref.plan) / ref.plan)
+    assert rel <= 1e-12, f"f64 plan differs by {rel:.3e}"
+    np.testing.assert_allclose(res.factors.beta, ref.beta, rtol=1e-12)
+
+
+def test_group_device_list_must_match_ranks(gpu):
+    uot = gpu
+    with pytest.raises(uot.InvalidParameter):
+        uot.SessionGroup(100, 100, 3, devices=[0, 0])

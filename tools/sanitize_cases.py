@@ -1,0 +1,41 @@
+"""Small solves through every device path, for compute-sanitizer runs
+(memcheck / racecheck / synccheck / initcheck). Results are checked against the
+oracle so a sanitizer-perturbed run that computes garbage also fails.
+
+compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+"""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import oracle  # noqa: E402  (test infrastructure: the checker)
+from paper_2412_11079_b200 import uot  # noqa: E402
+
+o = oracle.Oracle()
+KN = 1e-300
+
+
+def check(name, plan, ref):
+    rel = float(np.max(np.abs(plan.astype(np.float64) - ref) / ref))
+    print(f"{name:40s} max rel err {rel:.2e}", flush=True)
+    if rel > 1e-5:
+        raise SystemExit(f"{name}: parity failed")
+
+
+cases = [(40, 3000, 4), (24, 20000, 3), (96, 1000, 5), (7, 9, 3)]  # G=1 streaming, G>1, resident, tiny
+for m, n, k in cases:
+    a, rpd, cpd = o.gen_problem(42, m, n)
+    ref = o.fused_solve(a, rpd, cpd, 1.0, 0.1, KN, k, workers=2)
+    res = uot.fused_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KN, k)
+    with uot.Session(m, n) as s:
+        lay = s.layout
+    check(f"fused {m}x{n} G={lay['G']} resident={lay['resident']}", res.plan, ref.plan)
+a, rpd, cpd = o.gen_problem(3, 50, 2500, dtype=np.float64)
+ref = o.fused_solve(a, rpd, cpd, 1.0, 0.1, KN, 3, 2)
+check("f64 50x2500", uot.fused_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KN, 3).plan, ref.plan)
+a, rpd, cpd = o.gen_problem(5, 60, 1500)
+ref = o.distributed_solve(a, rpd, cpd, 1.0, 0.1, KN, 3, 2)
+check("2-rank group 60x1500", uot.distributed_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KN, 3, 2, devices=[0, 0]).plan,
+      ref.plan)
+print("sanitize cases OK")
