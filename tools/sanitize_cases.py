@@ -23,19 +23,22 @@ def check(name, plan, ref):
         raise SystemExit(f"{name}: parity failed")
 
 
-cases = [(40, 3000, 4), (24, 20000, 3), (96, 1000, 5), (7, 9, 3)]  # G=1 streaming, G>1, resident, tiny
+# streaming G=1 (34 rows per CTA: not resident), G=3, G=4 with TMEM column
+# factors, resident, tiny
+cases = [(5100, 1000, 3), (24, 20000, 3), (40, 32768, 3), (96, 1000, 5), (7, 9, 3)]
 for m, n, k in cases:
     a, rpd, cpd = o.gen_problem(42, m, n)
     ref = o.fused_solve(a, rpd, cpd, 1.0, 0.1, KN, k, workers=2)
     res = uot.fused_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KN, k)
     with uot.Session(m, n) as s:
         lay = s.layout
-    check(f"fused {m}x{n} G={lay['G']} resident={lay['resident']}", res.plan, ref.plan)
+    check(f"fused {m}x{n} G={lay['G']} resident={lay['resident']} v={lay['chunks']}", res.plan, ref.plan)
 a, rpd, cpd = o.gen_problem(3, 50, 2500, dtype=np.float64)
 ref = o.fused_solve(a, rpd, cpd, 1.0, 0.1, KN, 3, 2)
 check("f64 50x2500", uot.fused_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KN, 3).plan, ref.plan)
-a, rpd, cpd = o.gen_problem(5, 60, 1500)
-ref = o.distributed_solve(a, rpd, cpd, 1.0, 0.1, KN, 3, 2)
-check("2-rank group 60x1500", uot.distributed_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KN, 3, 2, devices=[0, 0]).plan,
-      ref.plan)
+for (m, n) in [(60, 1500), (64, 16384)]:  # group ranks at G=1 and G=2 (smid-addressed CTAs)
+    a, rpd, cpd = o.gen_problem(5, m, n)
+    ref = o.distributed_solve(a, rpd, cpd, 1.0, 0.1, KN, 3, 2)
+    check(f"2-rank group {m}x{n}",
+          uot.distributed_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KN, 3, 2, devices=[0, 0]).plan, ref.plan)
 print("sanitize cases OK")
