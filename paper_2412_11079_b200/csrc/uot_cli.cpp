@@ -3,8 +3,10 @@
 // the C ABI (include/uot_cuda.h). Same options, same JSON report keys
 // (report_json, uot_main.cpp:118-130), same CSV header (uot_main.cpp:340), same
 // exit codes (0 converged, 2 not converged, 1 error). Solvers: `cuda` (the
-// fused sweep; `fused` and `parallel` are accepted as aliases), and the GPU
-// ablations `baseline` (baseline.hpp) and `tiled` (tiled.hpp two-pass).
+// fused sweep; `fused` and `parallel` are accepted as aliases), the GPU
+// ablations `baseline` (baseline.hpp) and `tiled` (tiled.hpp two-pass), and
+// `dist --ranks P` (uot_main.cpp:109-111, distributed_solve): P row-sharded
+// ranks in this process over the visible GPUs (uot_create_group).
 #include <cerrno>
 #include <chrono>
 #include <cmath>
@@ -118,6 +120,61 @@ Report run(uot_ctx* ctx, const std::string& solver, double tol, uint64_t max_ite
   return r;
 }
 
+// --solver dist: distributed_solve(p, tol, max_iter, ranks) (uot_main.cpp:109-111)
+// as an in-process session group, rank r on --devices[r] (default: round robin).
+struct Group {
+  std::vector<uot_ctx*> ctx;
+  ~Group() {
+    for (auto* c : ctx) uot_destroy(c);
+  }
+  void check(int rc) const {
+    if (rc == UOT_OK) return;
+    std::string msg = "session group";
+    for (auto* c : ctx)
+      if (c && *uot_last_error(c)) msg = uot_last_error(c);
+    throw Fail{rc, msg};
+  }
+};
+
+Report run_dist(const Args& a, Group& g, uint64_t& m, uint64_t& n, int& dtype, double tol, uint64_t max_iter) {
+  if (!(tol > 0.0)) throw Fail{UOT_INVALID_PARAMETER, "tol must be positive"};
+  if (max_iter < 1) throw Fail{UOT_INVALID_PARAMETER, "max_iter must be at least 1"};
+  const uint64_t ranks = a.u64("ranks", 2);  // uot_main.cpp:216 default
+  if (ranks < 1 || ranks > 4096) throw Fail{UOT_PARTITION_ERROR, "RankPartition: ranks must be in [1, 4096]"};
+  std::string path;
+  if (a.has("in")) {
+    path = a.kv.at("in");
+    double er = 0, ep = 0;
+    const int rc = uot_problem_file_info(path.c_str(), &m, &n, &dtype, &er, &ep);
+    if (rc) throw Fail{rc, uot_last_io_error()};
+  } else {
+    m = a.u64("m", 64);
+    n = a.u64("n", 64);
+    dtype = parse_dtype(a.str("dtype", "fp64"));
+  }
+  std::vector<int> dev;
+  if (a.has("devices")) {
+    std::stringstream ss(a.kv.at("devices"));
+    std::string t;
+    while (std::getline(ss, t, ',')) dev.push_back(std::atoi(t.c_str()));
+    if (dev.size() != ranks) throw Fail{UOT_INVALID_PARAMETER, "--devices needs one device per rank"};
+  }
+  g.ctx.assign(ranks, nullptr);
+  g.check(uot_create_group(g.ctx.data(), m, n, dtype, dev.empty() ? nullptr : dev.data(), static_cast<int>(ranks),
+                           nullptr));
+  for (auto* c : g.ctx)  // each rank streams / generates only its row block
+    g.check(path.empty() ? uot_generate_problem(c, a.u64("seed", 1), 1.0, 1.0) : uot_load_problem_file(c, path.c_str()));
+  const auto t0 = std::chrono::steady_clock::now();
+  g.check(uot_group_init_col_sums(g.ctx.data(), static_cast<int>(ranks)));
+  Report r;
+  int conv = 0;
+  g.check(uot_group_iterate(g.ctx.data(), static_cast<int>(ranks), max_iter, tol, &r.iterations, &r.final_error, &conv));
+  r.converged = conv != 0;
+  r.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  r.solver = "dist";
+  return r;
+}
+
 // write_problem's container (problem_io.cpp:97-104) straight from the host generator.
 void write_generated(const std::string& path, uint64_t seed, uint64_t m, uint64_t n, int dtype) {
   const size_t es = dtype == UOT_F64 ? 8 : 4;
@@ -145,8 +202,9 @@ void usage() {
   std::puts(
       "uot-cuda: the reference CLI (tools/uot_main.cpp) on a B200\n"
       "  gen   --out FILE [--seed S] [--m M] [--n N] [--dtype fp32|fp64]\n"
-      "  solve [--in FILE | --seed S --m M --n N --dtype fp32|fp64] [--solver cuda|baseline|tiled]\n"
+      "  solve [--in FILE | --seed S --m M --n N --dtype fp32|fp64] [--solver cuda|baseline|tiled|dist]\n"
       "        [--tol T] [--max-iter K] [--out REPORT.json] [--plan-out FILE] [--device D]\n"
+      "        [--ranks P [--devices 0,1,..]]   (dist: P row-sharded ranks over the GPUs)\n"
       "  bench [--sizes 256,512,1024] [--solvers cuda,baseline] [--iters K] [--seed S] [--dtype fp32|fp64]\n"
       "        [--out FILE.csv] [--device D]\n"
       "exit: 0 ok / converged, 2 not converged, 1 error");
@@ -176,6 +234,22 @@ int main(int argc, char** argv) {
       write_generated(a.kv.at("out"), a.u64("seed", 1), a.u64("m", 64), a.u64("n", 64),
                       parse_dtype(a.str("dtype", "fp64")));
       return 0;
+    }
+    if (cmd == "solve" && a.str("solver", "cuda") == "dist") {
+      Group g;
+      uint64_t m = 0, n = 0;
+      int dt = UOT_F32;
+      const Report r = run_dist(a, g, m, n, dt, a.f64("tol", 1e-6), a.u64("max-iter", 10000));
+      if (a.has("plan-out"))
+        for (auto* c : g.ctx) g.check(uot_save_problem_file(c, a.kv.at("plan-out").c_str()));
+      std::ostringstream js;  // report_json (uot_main.cpp:118-130)
+      js << "{\n  \"solver\": \"dist\",\n  \"M\": " << m << ",\n  \"N\": " << n << ",\n  \"dtype\": \""
+         << dtype_name(dt) << "\",\n  \"workers\": 1,\n  \"ranks\": " << g.ctx.size() << ",\n"
+         << "  \"iterations\": " << r.iterations << ",\n  \"final_error\": " << num(r.final_error)
+         << ",\n  \"converged\": " << (r.converged ? "true" : "false") << ",\n  \"wall_ms\": " << num(r.wall_ms)
+         << "\n}\n";
+      emit(js.str(), a.str("out", ""));
+      return r.converged ? 0 : 2;
     }
     if (cmd == "solve") {
       Loaded L;

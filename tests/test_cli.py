@@ -86,3 +86,30 @@ def test_bench_csv(gpu, cli):
     assert lines[0] == "M,N,solver,workers,iterations,wall_ms,bytes_modeled"
     rows = [l.split(",") for l in lines[1:]]
     assert len(rows) == 6 and all(int(x[4]) == 5 and float(x[5]) > 0 for x in rows)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["fp32", "fp64"])
+def test_solve_dist_matches_distributed_solve(gpu, cli, orc, tmp_path, dtype):
+    # uot_main.cpp:109-111: --solver dist --ranks P -> distributed_solve(p, tol, max_iter, P)
+    src, plan_out = tmp_path / "p.uotp", tmp_path / "plan.uotp"
+    assert run(cli, "gen", "--out", src, "--seed", 6, "--m", 301, "--n", 3000, "--dtype", dtype).returncode == 0
+    r = run(cli, "solve", "--in", src, "--solver", "dist", "--ranks", 3, "--devices", "0,0,0", "--tol", KNEVER,
+            "--max-iter", 7, "--plan-out", plan_out)
+    assert r.returncode == 2, r.stderr
+    d = json.loads(r.stdout)
+    assert d["solver"] == "dist" and d["ranks"] == 3 and d["iterations"] == 7 and d["dtype"] == dtype
+    a, rpd, cpd = orc.gen_problem(6, 301, 3000, dtype=np.float64 if dtype == "fp64" else np.float32)
+    if dtype == "fp32":
+        ref = orc.distributed_solve(a, rpd, cpd, 1.0, 1.0, KNEVER, 7, 3)
+    else:
+        ref = orc.fused_solve(a, rpd, cpd, 1.0, 1.0, KNEVER, 7, 3)  # (= distributed_solve, test_distributed.cpp)
+    assert abs(d["final_error"] - ref.final_error) <= 1e-9 * max(1.0, ref.final_error)
+    back = gpu.read_problem(plan_out)
+    rel = np.max(np.abs(back.a.astype(np.float64) - ref.plan) / ref.plan)
+    assert rel <= (1e-12 if dtype == "fp64" else 1e-5)
+    # generated in HBM per rank, more ranks than rows -> PartitionError (exit 1)
+    g = run(cli, "solve", "--seed", 2, "--m", 100, "--n", 500, "--dtype", dtype, "--solver", "dist", "--ranks", 2,
+            "--devices", "0,0", "--max-iter", 3, "--tol", KNEVER)
+    assert g.returncode == 2 and json.loads(g.stdout)["ranks"] == 2
+    assert run(cli, "solve", "--m", 3, "--n", 8, "--solver", "dist", "--ranks", 4).returncode == 1
