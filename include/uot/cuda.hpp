@@ -216,19 +216,24 @@ inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t m
 }
 
 namespace detail {
-inline SolveResult<float> solve_with(const Problem<float>& p, double tol, std::size_t max_iter, int device,
-                                     int variant, const char* solver, const char* who) {
+template <typename T>
+inline SolveResult<T> solve_with(const Problem<T>& p, double tol, std::size_t max_iter, int device, int variant,
+                                 const char* solver, const char* who) {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "Problem<float> or Problem<double>");
   require_valid(p);
   if (!(tol > 0.0)) throw InvalidParameter(std::string(who) + ": tol must be positive");
   if (max_iter < 1) throw InvalidParameter(std::string(who) + ": max_iter must be at least 1");
   const auto t0 = std::chrono::steady_clock::now();
-  Session s(p.m(), p.n(), device);
+  Session s(p.m(), p.n(), device, std::is_same_v<T, double> ? Dtype::f64 : Dtype::f32);
   s.set_problem(p);
   s.init_col_sums();
   s.set_variant(variant);
   const auto pr = s.iterate(max_iter, tol);
-  SolveResult<float> r;
-  r.plan = s.plan();
+  SolveResult<T> r;
+  if constexpr (std::is_same_v<T, double>)
+    r.plan = s.plan_f64();
+  else
+    r.plan = s.plan();
   r.factors = s.factors();
   r.report.solver = solver;
   r.report.iterations = pr.iterations;
@@ -242,14 +247,15 @@ inline SolveResult<float> solve_with(const Problem<float>& p, double tol, std::s
 
 // baseline_solve (baseline.hpp:118-142): the four-sweep schedule on the GPU
 // (an ablation of the fused sweep: 3x its HBM traffic).
-inline SolveResult<float> baseline_solve(const Problem<float>& p, double tol, std::size_t max_iter,
-                                         int device = 0) {
+template <typename T>
+inline SolveResult<T> baseline_solve(const Problem<T>& p, double tol, std::size_t max_iter, int device = 0) {
   return detail::solve_with(p, tol, max_iter, device, UOT_VARIANT_BASELINE, "baseline", "baseline_solve");
 }
 
 // tiled_solve (tiled.hpp:231-260): the paper's two-pass GPU data flow (part4 ->
 // row factors -> part2); the reference's TileConfig shapes have no meaning here.
-inline SolveResult<float> tiled_solve(const Problem<float>& p, double tol, std::size_t max_iter, int device = 0) {
+template <typename T>
+inline SolveResult<T> tiled_solve(const Problem<T>& p, double tol, std::size_t max_iter, int device = 0) {
   return detail::solve_with(p, tol, max_iter, device, UOT_VARIANT_TWO_PASS, "tiled", "tiled_solve");
 }
 

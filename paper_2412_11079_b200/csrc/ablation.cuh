@@ -18,6 +18,8 @@
 // float4 column chunks of a row block and keep the f64 column partials in
 // registers, written to a [row blocks][pitch] table the finalize kernel reduces.
 #pragma once
+#include <type_traits>
+
 #include "sweep.cuh"
 
 namespace uotk {
@@ -27,7 +29,7 @@ constexpr int kAblColThreads = 256;
 constexpr int kAblColV = 4;      // float4 chunks per thread: 4096 columns per CTA
 
 struct AblArgs {
-  float* P;
+  void* P;               // [rows][pitch] float (Problem<float>) or double (Problem<double>)
   const double* beta2;   // [2][pitch]
   const double* rpd;
   double* alpha;
@@ -70,7 +72,9 @@ __device__ __forceinline__ bool abl_stopped(Control* ctl, bool check_beta) {
 // s = sum_j f64(x) -> alpha_i = rescale_factor(rpd_i, s, fi) (fused.hpp:133 /
 // baseline.hpp:65-76). SCALE_ALPHA: x <- f32(f64(x)*alpha_i) (baseline row
 // scaling, baseline.hpp:78-88).
-template <bool SCALE_BETA, bool SUM, bool SCALE_ALPHA>
+// T = double (Problem<double>): the same schedule on plain f64 products, one
+// element per lane step (the f64 ablations exist for parity / verify).
+template <bool SCALE_BETA, bool SUM, bool SCALE_ALPHA, typename T = float>
 __global__ void __launch_bounds__(32 * kAblRowWarps) abl_row_kernel(const AblArgs a) {
   Control* ctl = a.ctl;
   if (abl_stopped(ctl, SCALE_BETA)) return;
@@ -79,11 +83,21 @@ __global__ void __launch_bounds__(32 * kAblRowWarps) abl_row_kernel(const AblArg
   __shared__ double werr[kAblRowWarps];
   double err = 0.0;
   if (i < a.rows) {
-    float4* row = reinterpret_cast<float4*>(a.P + i * a.pitch);
     const double* beta = a.beta2 + ((ctl->iter + 1) & 1ull) * a.pitch;
-    const unsigned nq = (a.cols + 3) / 4;
     double s = 0.0;
     double al = SCALE_ALPHA ? a.alpha[i] : 1.0;
+    if constexpr (std::is_same<T, double>::value) {
+      double* row = static_cast<double*>(a.P) + i * a.pitch;
+      for (unsigned j = lane; j < a.cols; j += 32) {
+        double x = row[j];
+        if (SCALE_BETA) x *= beta[j];
+        if (SCALE_ALPHA) x *= al;
+        if (SCALE_BETA || SCALE_ALPHA) row[j] = x;
+        if (SUM) s += x;
+      }
+    } else {
+    float4* row = reinterpret_cast<float4*>(static_cast<float*>(a.P) + i * a.pitch);
+    const unsigned nq = (a.cols + 3) / 4;
     for (unsigned q = lane; q < nq; q += 32) {
       float4 v = row[q];
       double d[4];
@@ -103,6 +117,7 @@ __global__ void __launch_bounds__(32 * kAblRowWarps) abl_row_kernel(const AblArg
         for (int e = 0; e < 4; ++e)
           if (4 * q + e < a.cols) s += d[e];
       }
+    }
     }
     if (SUM) {
       s = warp_sum(s);
@@ -132,7 +147,7 @@ __global__ void __launch_bounds__(32 * kAblRowWarps) abl_row_kernel(const AblArg
 // f32(f64(x)*beta_j) (baseline column scaling, baseline.hpp:48-56). SUM: column
 // partials of the (scaled) values -> partials[by][j] (baseline.hpp:30-38 /
 // fused.hpp:135-142).
-template <bool SCALE_ALPHA, bool SCALE_BETA, bool SUM>
+template <bool SCALE_ALPHA, bool SCALE_BETA, bool SUM, typename T = float>
 __global__ void __launch_bounds__(kAblColThreads) abl_col_kernel(const AblArgs a) {
   Control* ctl = a.ctl;
   if (abl_stopped(ctl, SCALE_BETA)) return;
@@ -152,11 +167,44 @@ __global__ void __launch_bounds__(kAblColThreads) abl_col_kernel(const AblArgs a
     for (int k = 0; k < V; ++k) {
       const unsigned q = q0 + k * kAblColThreads;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) beta[4 * k + e] = q < nq ? b[4 * q + e] : 0.0;
+      for (int e = 0; e < 4; ++e) beta[4 * k + e] = 4 * q + e < a.pitch ? b[4 * q + e] : 0.0;
     }
   }
+  if constexpr (std::is_same<T, double>::value) {  // 4 scalar columns per chunk, bounds per element
+    for (unsigned long long i = r0; i < r1; ++i) {
+      double* row = static_cast<double*>(a.P) + i * a.pitch;
+      const double al = SCALE_ALPHA ? a.alpha[i] : 1.0;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const unsigned q = q0 + k * kAblColThreads;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const unsigned j = 4 * q + e;
+          if (j < a.pitch) {
+            double x = row[j];
+            if (SCALE_ALPHA || SCALE_BETA) {
+              x *= SCALE_ALPHA ? al : beta[4 * k + e];
+              row[j] = x;
+            }
+            if (SUM) acc[4 * k + e] += x;
+          }
+        }
+      }
+    }
+    if (SUM) {
+      double* dst = a.partials + static_cast<size_t>(by) * a.pitch;
+#pragma unroll
+      for (int k = 0; k < V; ++k)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const unsigned j = 4 * (q0 + k * kAblColThreads) + e;
+          if (j < a.pitch) dst[j] = acc[4 * k + e];
+        }
+    }
+    return;
+  }
   for (unsigned long long i = r0; i < r1; ++i) {
-    float4* row = reinterpret_cast<float4*>(a.P + i * a.pitch);
+    float4* row = reinterpret_cast<float4*>(static_cast<float*>(a.P) + i * a.pitch);
     const double al = SCALE_ALPHA ? a.alpha[i] : 1.0;
     float4 v[V];
 #pragma unroll

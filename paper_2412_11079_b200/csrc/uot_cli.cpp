@@ -6,7 +6,9 @@
 // fused sweep; `fused` and `parallel` are accepted as aliases), the GPU
 // ablations `baseline` (baseline.hpp) and `tiled` (tiled.hpp two-pass), and
 // `dist --ranks P` (uot_main.cpp:109-111, distributed_solve): P row-sharded
-// ranks in this process over the visible GPUs (uot_create_group).
+// ranks in this process over the visible GPUs (uot_create_group). `verify`
+// (uot_main.cpp:131-175) runs them all and compares the plans with baseline's.
+#include <algorithm>
 #include <cerrno>
 #include <chrono>
 #include <cmath>
@@ -175,6 +177,70 @@ Report run_dist(const Args& a, Group& g, uint64_t& m, uint64_t& n, int& dtype, d
   return r;
 }
 
+// The plan of a session (its rows) as doubles.
+void plan_into(uot_ctx* ctx, int dtype, uint64_t rows, uint64_t n, double* out) {
+  if (dtype == UOT_F64) {
+    check(ctx, uot_get_plan_f64(ctx, out));
+    return;
+  }
+  std::vector<float> f(rows * n);
+  check(ctx, uot_get_plan(ctx, f.data()));
+  for (size_t k = 0; k < f.size(); ++k) out[k] = f[k];
+}
+
+double max_abs_diff(const std::vector<double>& a, const std::vector<double>& b) {  // matrix.hpp:66-73
+  double m = 0.0;
+  for (size_t k = 0; k < a.size(); ++k) m = std::max(m, std::fabs(a[k] - b[k]));
+  return m;
+}
+
+// verify (uot_main.cpp:131-175): every solver for a fixed iteration count on
+// the same problem, plans compared with the baseline's.
+std::string verify(const Args& a, int device, bool& ok) {
+  const uint64_t iters = a.u64("iters", 25), workers = a.u64("workers", 4), ranks = a.u64("ranks", 3);
+  const double tol = a.f64("tol", 1e-10);
+  std::map<std::string, std::vector<double>> plans;
+  uint64_t m = 0, n = 0;
+  int dt = UOT_F64;
+  for (const char* solver : {"baseline", "fused", "parallel", "tiled"}) {
+    Loaded L;
+    load(a, L, device);
+    m = L.m, n = L.n, dt = L.dtype;
+    run(L.ctx, solver, 1e-300, iters);
+    std::vector<double> p(m * n);
+    plan_into(L.ctx, dt, m, n, p.data());
+    plans[solver] = std::move(p);
+  }
+  const uint64_t eff_ranks = std::min<uint64_t>(ranks, m);
+  {
+    Args b = a;
+    b.kv["ranks"] = std::to_string(eff_ranks);
+    b.kv.erase("devices");
+    Group g;
+    uint64_t mm = 0, nn = 0;
+    int dd = 0;
+    run_dist(b, g, mm, nn, dd, 1e-300, iters);
+    std::vector<double> p(m * n);
+    for (auto* c : g.ctx) {
+      uot_layout l{};
+      g.check(uot_get_layout(c, &l));
+      plan_into(c, dt, l.rows, n, p.data() + l.row_offset * n);
+    }
+    plans["dist"] = std::move(p);
+  }
+  const auto& base = plans["baseline"];
+  const double d_fused = max_abs_diff(base, plans["fused"]), d_par = max_abs_diff(base, plans["parallel"]),
+               d_tiled = max_abs_diff(base, plans["tiled"]), d_dist = max_abs_diff(base, plans["dist"]);
+  const double d_max = std::max({d_fused, d_par, d_tiled, d_dist});
+  ok = d_max <= tol;
+  std::ostringstream js;
+  js << "{\n  \"iterations\": " << iters << ",\n  \"workers\": " << workers << ",\n  \"ranks\": " << eff_ranks
+     << ",\n  \"diff_vs_baseline\": {\n    \"fused\": " << num(d_fused) << ",\n    \"parallel\": " << num(d_par)
+     << ",\n    \"tiled\": " << num(d_tiled) << ",\n    \"dist\": " << num(d_dist) << "\n  },\n  \"max_diff\": "
+     << num(d_max) << ",\n  \"tolerance\": " << num(tol) << ",\n  \"ok\": " << (ok ? "true" : "false") << "\n}\n";
+  return js.str();
+}
+
 // write_problem's container (problem_io.cpp:97-104) straight from the host generator.
 void write_generated(const std::string& path, uint64_t seed, uint64_t m, uint64_t n, int dtype) {
   const size_t es = dtype == UOT_F64 ? 8 : 4;
@@ -205,6 +271,8 @@ void usage() {
       "  solve [--in FILE | --seed S --m M --n N --dtype fp32|fp64] [--solver cuda|baseline|tiled|dist]\n"
       "        [--tol T] [--max-iter K] [--out REPORT.json] [--plan-out FILE] [--device D]\n"
       "        [--ranks P [--devices 0,1,..]]   (dist: P row-sharded ranks over the GPUs)\n"
+      "  verify [--in FILE | --seed S --m M --n N --dtype fp32|fp64] [--iters 25] [--workers 4] [--ranks 3]\n"
+      "        [--tol 1e-10] [--out REPORT.json] [--device D]   (every solver vs baseline: exit 0 ok, 2 not)\n"
       "  bench [--sizes 256,512,1024] [--solvers cuda,baseline] [--iters K] [--seed S] [--dtype fp32|fp64]\n"
       "        [--out FILE.csv] [--device D]\n"
       "exit: 0 ok / converged, 2 not converged, 1 error");
@@ -264,6 +332,11 @@ int main(int argc, char** argv) {
          << ",\n  \"device_ms\": " << num(r.device_ms) << "\n}\n";
       emit(js.str(), a.str("out", ""));
       return r.converged ? 0 : 2;
+    }
+    if (cmd == "verify") {
+      bool ok = false;
+      emit(verify(a, device, ok), a.str("out", ""));
+      return ok ? 0 : 2;
     }
     if (cmd == "bench") {
       std::vector<uint64_t> sizes;

@@ -565,7 +565,7 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
 // ------------------------------------------------------------ ablations --
 AblArgs abl_args(const uot_ctx* ctx) {
   AblArgs a;
-  a.P = ctx->Pf();
+  a.P = ctx->P;
   a.beta2 = ctx->beta2;
   a.rpd = ctx->rpd;
   a.alpha = ctx->alpha;
@@ -591,25 +591,33 @@ FinalizeArgs abl_fin_args(const uot_ctx* ctx) {
 
 // One iteration of the two-pass (tiled.hpp:210-229) or four-sweep baseline
 // (baseline.hpp:100-110) schedule; see ablation.cuh.
-int launch_ablation_iteration(uot_ctx* ctx) {
+template <typename T>
+void launch_ablation_kernels(uot_ctx* ctx) {
   const AblArgs a = abl_args(ctx);
   const dim3 cg(ctx->abl_gx, ctx->abl_gy);
   const unsigned rg = ctx->abl_rowctas, rt = 32 * kAblRowWarps;
   const unsigned fb = finalize_blocks(ctx->pitch);
   if (ctx->variant == UOT_VARIANT_TWO_PASS) {
-    abl_row_kernel<true, true, false><<<rg, rt, 0, ctx->stream>>>(a);          // part4 -> alpha
-    abl_col_kernel<true, false, true><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // part2 -> column partials
+    abl_row_kernel<true, true, false, T><<<rg, rt, 0, ctx->stream>>>(a);          // part4 -> alpha
+    abl_col_kernel<true, false, true, T><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // part2 -> column partials
     finalize_kernel<kFinIter, true, true><<<fb, kFinThreads, 0, ctx->stream>>>(abl_fin_args(ctx));
     ctx->launches += 3;
   } else {
-    abl_col_kernel<false, false, true><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // column sums
+    abl_col_kernel<false, false, true, T><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // column sums
     finalize_kernel<kFinSeed, true, true><<<fb, kFinThreads, 0, ctx->stream>>>(abl_fin_args(ctx));  // beta(t)
-    abl_col_kernel<false, true, false><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // column scaling
-    abl_row_kernel<false, true, false><<<rg, rt, 0, ctx->stream>>>(a);             // row sums -> alpha
-    abl_row_kernel<false, false, true><<<rg, rt, 0, ctx->stream>>>(a);             // row scaling
+    abl_col_kernel<false, true, false, T><<<cg, kAblColThreads, 0, ctx->stream>>>(a);  // column scaling
+    abl_row_kernel<false, true, false, T><<<rg, rt, 0, ctx->stream>>>(a);             // row sums -> alpha
+    abl_row_kernel<false, false, true, T><<<rg, rt, 0, ctx->stream>>>(a);             // row scaling
     abl_baseline_tail_kernel<<<1, 256, 0, ctx->stream>>>(a, rg);
     ctx->launches += 6;
   }
+}
+
+int launch_ablation_iteration(uot_ctx* ctx) {
+  if (ctx->dtype == UOT_F64)
+    launch_ablation_kernels<double>(ctx);
+  else
+    launch_ablation_kernels<float>(ctx);
   return ctx->cuda(cudaGetLastError(), "ablation launch");
 }
 
@@ -954,11 +962,9 @@ int uot_set_variant(uot_ctx* ctx, int variant) {
     return ctx->fail(UOT_INVALID_PARAMETER, "unknown iteration variant %d", variant);
   if (variant != UOT_VARIANT_FUSED && ctx->nranks > 1)
     return ctx->fail(UOT_INVALID_PARAMETER, "the ablation schedules are single-GPU only");
-  if (variant != UOT_VARIANT_FUSED && ctx->dtype != UOT_F32)
-    return ctx->fail(UOT_INVALID_PARAMETER, "the ablation schedules are fp32 only");
   CK(cudaSetDevice(ctx->device));
   if (variant != UOT_VARIANT_FUSED && !ctx->abl_partials) {
-    ctx->abl_gx = (ctx->pitch / 4 + kAblColThreads * kAblColV - 1) / (kAblColThreads * kAblColV);
+    ctx->abl_gx = ((ctx->pitch + 3) / 4 + kAblColThreads * kAblColV - 1) / (kAblColThreads * kAblColV);
     ctx->abl_gy = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>(ctx->rows, (4u * ctx->sms + ctx->abl_gx - 1) / ctx->abl_gx)));
     ctx->abl_rowctas = static_cast<unsigned>((ctx->rows + kAblRowWarps - 1) / kAblRowWarps);

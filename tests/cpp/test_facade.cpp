@@ -194,6 +194,17 @@ void test_f64_problem_matches_reference() {  // Problem<double>, Dtype::f64
     m = std::max(m, std::abs(gpu.plan.data()[k] - ref.plan.data()[k]) / ref.plan.data()[k]);
   CHECK(m <= 1e-12);
   CHECK(uot::max_abs_diff(gpu.factors.beta, ref.factors.beta) <= 1e-12);
+  const auto rb = uot::baseline_solve(p, kNever, 7);  // the f64 ablations (baseline.hpp / tiled.hpp, T = double)
+  const auto gb = uot::cuda::baseline_solve(p, kNever, 7);
+  const auto gt = uot::cuda::tiled_solve(p, kNever, 7);
+  const auto rt = uot::fused_solve(p, kNever, 7, std::size_t(2));
+  double mb = 0.0, mt = 0.0;
+  for (std::size_t k = 0; k < gb.plan.size(); ++k) {
+    mb = std::max(mb, std::abs(gb.plan.data()[k] - rb.plan.data()[k]) / rb.plan.data()[k]);
+    mt = std::max(mt, std::abs(gt.plan.data()[k] - rt.plan.data()[k]) / rt.plan.data()[k]);
+  }
+  CHECK(gb.report.iterations == 7 && mb <= 1e-12);
+  CHECK(gt.report.iterations == 7 && mt <= 1e-12);
 }
 
 void test_single_rank_peer_distributed() {

@@ -113,3 +113,20 @@ def test_solve_dist_matches_distributed_solve(gpu, cli, orc, tmp_path, dtype):
             "--devices", "0,0", "--max-iter", 3, "--tol", KNEVER)
     assert g.returncode == 2 and json.loads(g.stdout)["ranks"] == 2
     assert run(cli, "solve", "--m", 3, "--n", 8, "--solver", "dist", "--ranks", 4).returncode == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,tol", [("fp64", None), ("fp32", 1e-6)])
+def test_verify_every_solver_agrees_with_baseline(gpu, cli, dtype, tol):
+    # uot_main.cpp:131-175: fused / parallel / tiled / dist vs baseline after --iters iterations
+    args = ["verify", "--seed", 5, "--m", 130, "--n", 900, "--dtype", dtype, "--iters", 12, "--ranks", 3]
+    if tol is not None:
+        args += ["--tol", tol]
+    r = run(cli, *args)
+    d = json.loads(r.stdout)
+    assert set(d) == {"iterations", "workers", "ranks", "diff_vs_baseline", "max_diff", "tolerance", "ok"}
+    assert set(d["diff_vs_baseline"]) == {"fused", "parallel", "tiled", "dist"}
+    assert d["iterations"] == 12 and d["ranks"] == 3 and d["ok"] and r.returncode == 0, r.stdout + r.stderr
+    assert d["max_diff"] <= (1e-10 if dtype == "fp64" else 1e-6)
+    bad = run(cli, "verify", "--seed", 5, "--m", 130, "--n", 900, "--dtype", dtype, "--iters", 3, "--tol", -1)
+    assert bad.returncode == 2 and not json.loads(bad.stdout)["ok"]  # tolerance not met -> exit 2

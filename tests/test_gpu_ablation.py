@@ -64,3 +64,23 @@ def test_unknown_variant_rejected(gpu):
     with gpu.Session(8, 8) as s:
         with pytest.raises(gpu.InvalidParameter):
             s.set_variant("three_pass")
+
+
+@pytest.mark.parametrize("m,n,k", [(300, 2000, 8), (257, 4098, 5), (7, 3, 11), (64, 9001, 4)])
+@pytest.mark.parametrize("variant", ["two_pass", "baseline"])
+def test_variant_f64_matches_oracle(gpu, orc, variant, m, n, k):
+    # Problem<double>: plain f64 products in every schedule (baseline.hpp / tiled.hpp with T = double);
+    # 4098 / 9001 columns leave a row pitch that is not a multiple of 4 (per-element bounds)
+    a, rpd, cpd = orc.gen_problem(43, m, n, dtype=np.float64)
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 2)
+    with gpu.Session(m, n, dtype=np.float64) as s:
+        s.set_problem(gpu.Problem(a, rpd, cpd, 1.0, 0.1))
+        s.init_col_sums()
+        s.set_variant(variant)
+        it, err, conv = s.iterate(k, KNEVER)
+        plan, f = s.plan(), s.factors()
+    assert it == k and plan.dtype == np.float64
+    rel = np.max(np.abs(plan - ref.plan) / ref.plan)
+    assert rel <= 1e-12, f"{variant} f64 {m}x{n}: {rel:.3e}"
+    np.testing.assert_allclose(f.beta, ref.beta, rtol=1e-12)
+    assert abs(err - ref.final_error) <= 1e-9 * max(1.0, ref.final_error)
