@@ -75,6 +75,8 @@ typedef struct uot_layout {
   int32_t persist;       /* otherwise, single rank: ONE persistent streaming launch (persist.cuh) */
   int32_t dtype;         /* UOT_F32 (Problem<float>) or UOT_F64 (Problem<double>) */
   int32_t dynamic;       /* 1: row batches handed out by a device counter (uot_set_deterministic) */
+  int32_t variant;       /* iteration schedule (UOT_VARIANT_*); rows wider than #SMs slices (G > #SMs,
+                            > 1.2M fp32 columns on a B200) run UOT_VARIANT_TWO_PASS, the only one they allow */
 } uot_layout;
 
 /* ---- sessions ---------------------------------------------------------- */

@@ -277,6 +277,7 @@ struct uot_ctx {
   int rfull = 0;
   bool use_tmem = false;  // iterations run sweep_tmem_kernel (opt-in: UOT_TMEM=1)
   bool use_persist = false;  // uot_iterate is one persistent streaming launch (persist.cuh, opt-in)
+  bool wide = false;  // rows wider than #SMs slices: only the two-pass schedule (ablation.cuh) runs
 
   // device buffers
   void* P = nullptr;          // [rows][pitch] of `dtype` (float or double)
@@ -365,9 +366,24 @@ int plan_layout(uot_ctx* ctx) {
   const unsigned smax = kSliceMax * 4 / ctx->esz;  // 32 KiB of elements
   const unsigned xmax = static_cast<unsigned>(env_int("UOT_SLICE_MAX_XCHG", kSliceMaxXchg)) * 4 / ctx->esz;
   unsigned G = cols <= smax ? 1u : static_cast<unsigned>((cols + xmax - 1) / xmax);
-  if (G > static_cast<unsigned>(ctx->sms))
-    return ctx->fail(UOT_CONFIG_ERROR, "cols %llu needs %u CTAs per row (max %d)",
-                     (unsigned long long)cols, G, ctx->sms);
+  if (G > static_cast<unsigned>(ctx->sms)) {
+    // Rows wider than one slice per SM: the fused sweep cannot hold a row across
+    // the grid, so a single-rank session runs the paper's two-pass schedule
+    // (ablation.cuh: warp-per-row and column kernels, any width, the same
+    // arithmetic at 16 B per element) for the seed and every iteration.
+    if (ctx->nranks > 1 || !env_int("UOT_WIDE", 1))
+      return ctx->fail(UOT_CONFIG_ERROR, "cols %llu needs %u CTAs per row (max %d)",
+                       (unsigned long long)cols, G, ctx->sms);
+    ctx->wide = true;
+    ctx->G = 1;
+    ctx->slice = ctx->pitch = round_up(static_cast<unsigned>(cols), 4);
+    ctx->cfg = &(f64 ? cfg_table_f64() : cfg_table()).front();  // (layout reporting only: no sweep launches)
+    ctx->B = 1;
+    ctx->groups = ctx->grid = 1;
+    ctx->buf_stride = 128;
+    ctx->dyn = 0;
+    return UOT_OK;
+  }
   const unsigned slice = round_up(static_cast<unsigned>((cols + G - 1) / G), epc);
   const SweepCfg* cfg = nullptr;
   for (const auto& c : f64 ? cfg_table_f64() : cfg_table())
@@ -488,7 +504,8 @@ int create_common(uot_ctx* ctx, int device) {
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   int rc = plan_layout(ctx);
   if (rc) return rc;
-  return alloc_all(ctx);
+  if ((rc = alloc_all(ctx))) return rc;
+  return ctx->wide ? uot_set_variant(ctx, UOT_VARIANT_TWO_PASS) : UOT_OK;
 }
 
 SweepArgs sweep_args(const uot_ctx* ctx) {
@@ -962,6 +979,9 @@ int uot_set_variant(uot_ctx* ctx, int variant) {
     return ctx->fail(UOT_INVALID_PARAMETER, "unknown iteration variant %d", variant);
   if (variant != UOT_VARIANT_FUSED && ctx->nranks > 1)
     return ctx->fail(UOT_INVALID_PARAMETER, "the ablation schedules are single-GPU only");
+  if (variant != UOT_VARIANT_TWO_PASS && ctx->wide)
+    return ctx->fail(UOT_CONFIG_ERROR, "rows of %llu columns exceed one slice per SM: two-pass schedule only",
+                     (unsigned long long)ctx->cols);
   CK(cudaSetDevice(ctx->device));
   if (variant != UOT_VARIANT_FUSED && !ctx->abl_partials) {
     ctx->abl_gx = ((ctx->pitch + 3) / 4 + kAblColThreads * kAblColV - 1) / (kAblColThreads * kAblColV);
@@ -1031,6 +1051,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->evict_first = ctx->evict_first;
   o->smid_map = ctx->smid_map;
   o->exchange = ctx->xmode;
+  o->variant = ctx->variant;
   return UOT_OK;
 }
 
@@ -1149,8 +1170,20 @@ int uot_init_col_sums(uot_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   int rc = reset_state(ctx);
   if (rc) return rc;
-  if ((rc = launch_sweep(ctx, /*seed=*/true))) return rc;
-  if ((rc = launch_finalize<kFinSeed>(ctx))) return rc;
+  if (ctx->wide) {  // column sums with the two-pass schedule's column kernel (baseline.hpp:30-38)
+    const dim3 cg(ctx->abl_gx, ctx->abl_gy);
+    if (ctx->dtype == UOT_F64)
+      abl_col_kernel<false, false, true, double><<<cg, kAblColThreads, 0, ctx->stream>>>(abl_args(ctx));
+    else
+      abl_col_kernel<false, false, true, float><<<cg, kAblColThreads, 0, ctx->stream>>>(abl_args(ctx));
+    finalize_kernel<kFinSeed, true, true><<<finalize_blocks(ctx->pitch), kFinThreads, 0, ctx->stream>>>(
+        abl_fin_args(ctx));
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+  } else {
+    if ((rc = launch_sweep(ctx, /*seed=*/true))) return rc;
+    if ((rc = launch_finalize<kFinSeed>(ctx))) return rc;
+  }
   if ((rc = sync_ctl(ctx))) return rc;
   ctx->seeded = true;
   return UOT_OK;

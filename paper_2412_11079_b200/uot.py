@@ -89,7 +89,7 @@ class Layout(C.Structure):
                 ("nranks", C.c_int32), ("device", C.c_int32), ("evict_first", C.c_int32),
                 ("smid_map", C.c_int32), ("exchange", C.c_int32), ("tmem", C.c_int32),
                 ("resident", C.c_int32), ("persist", C.c_int32), ("dtype", C.c_int32),
-                ("dynamic", C.c_int32)]
+                ("dynamic", C.c_int32), ("variant", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

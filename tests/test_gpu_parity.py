@@ -330,3 +330,25 @@ def test_randomized_shapes_against_oracle(gpu, orc):
         assert it == k, (case, m, n)
         assert_parity(plan, ref.plan, rpd, cpd, f"case {case}: {m}x{n} fi={fi} k={k} layout={lay}")
         assert abs(err - ref.final_error) <= 1e-9 * max(1.0, ref.final_error), (case, m, n)
+
+
+@pytest.mark.parametrize("m,n,dt", [(3, 148 * 8192 + 100, np.float32), (2, 148 * 4096 + 7, np.float64)])
+def test_rows_wider_than_the_grid_run_two_pass(gpu, orc, m, n, dt):
+    # G > #SMs: one row cannot span the sweep grid; the session runs the paper's
+    # two-pass schedule (tiled.hpp:210-229) for the seed and every iteration
+    uot = gpu
+    a, rpd, cpd = orc.gen_problem(21, m, n, dtype=dt)
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, 3, 1)
+    with uot.Session(m, n, dtype=dt) as s:
+        assert s.layout["variant"] == 1  # UOT_VARIANT_TWO_PASS
+        s.set_problem(uot.Problem(a, rpd, cpd, 1.0, 0.1))
+        s.init_col_sums()
+        np.testing.assert_allclose(s.col_sums(), a.astype(np.float64).sum(0), rtol=1e-12)
+        it, err, _ = s.iterate(3, KNEVER)
+        plan = s.plan()
+        with pytest.raises(uot.ConfigError):
+            s.set_variant("fused")
+    assert it == 3
+    rel = np.max(np.abs(plan.astype(np.float64) - ref.plan) / ref.plan)
+    assert rel <= (1e-12 if dt == np.float64 else 1e-5), rel
+    assert abs(err - ref.final_error) <= 1e-9 * max(1.0, ref.final_error)
