@@ -1,0 +1,67 @@
+"""Parity at the BASELINE configurations' FULL sizes and iteration counts:
+the GPU's fused_solve against the reference's own fused_solve (oracle/_ref:
+the reference compiled from its sources; the C restatement if absent), both
+from the same gen_problem_t<float>(42, R, C) with er = 1, ep = 0.1.
+
+Test infrastructure (it runs the checker), not a bench: the CPU leg is the
+reference's threaded fused_iterate_parallel over all host cores.
+
+python tools/full_parity.py [--only 1,2,3,4] [--json OUT]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import oracle  # noqa: E402
+from paper_2412_11079_b200 import uot  # noqa: E402
+
+CONFIGS = [(1, 1024, 1024, 100), (2, 8192, 8192, 500), (3, 32768, 32768, 200), (4, 262144, 4096, 200)]
+only = None
+if "--only" in sys.argv:
+    only = {int(x) for x in sys.argv[sys.argv.index("--only") + 1].split(",")}
+ref = oracle.RefOracle() if oracle.have_ref() else oracle.Oracle()
+kind = "reference (oracle/_ref)" if isinstance(ref, oracle.RefOracle) else "C restatement (oracle/uot_oracle.c)"
+gen = oracle.Oracle()
+threads = os.cpu_count() or 1
+rows = []
+for idx, m, n, k in CONFIGS:
+    if only and idx not in only:
+        continue
+    a, rpd, cpd = gen.gen_problem(42, m, n, threads=threads)
+    t0 = time.time()
+    r = ref.fused_solve(a, rpd, cpd, 1.0, 0.1, 1e-300, k, threads)
+    t_cpu = time.time() - t0
+    t0 = time.time()
+    g = uot.fused_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), 1e-300, k)
+    t_gpu = time.time() - t0
+    rel = np.abs(g.plan.astype(np.float64) - r.plan.astype(np.float64)) / r.plan.astype(np.float64)
+    row = {
+        "config": idx, "rows": m, "cols": n, "iterations": k, "checker": kind, "cpu_threads": threads,
+        "iterations_gpu": g.report.iterations, "iterations_ref": r.iterations,
+        "plan_max_rel_err": float(rel.max()),
+        "plan_bitwise_equal_fraction": float(np.mean(g.plan == r.plan)),
+        "alpha_max_rel_err": float(np.max(np.abs(g.factors.alpha - r.alpha) / r.alpha)),
+        "beta_max_rel_err": float(np.max(np.abs(g.factors.beta - r.beta) / r.beta)),
+        "final_error_gpu": g.report.final_error, "final_error_ref": r.final_error,
+        "row_marginal_err_gpu": float(np.max(np.abs(g.plan.sum(1, dtype=np.float64) - rpd) / rpd)),
+        "row_marginal_err_ref": float(np.max(np.abs(r.plan.sum(1, dtype=np.float64) - rpd) / rpd)),
+        "col_marginal_err_gpu": float(np.max(np.abs(g.plan.sum(0, dtype=np.float64) - cpd) / cpd)),
+        "col_marginal_err_ref": float(np.max(np.abs(r.plan.sum(0, dtype=np.float64) - cpd) / cpd)),
+        "wall_s_ref": t_cpu, "wall_s_gpu_incl_pcie": t_gpu,
+    }
+    ok = row["plan_max_rel_err"] <= 1e-5 and row["iterations_gpu"] == row["iterations_ref"]
+    row["within_1e-5"] = bool(ok)
+    rows.append(row)
+    print(f"config {idx} {m}x{n} K={k}: plan max rel {row['plan_max_rel_err']:.2e}, bitwise "
+          f"{row['plan_bitwise_equal_fraction'] * 100:.4f}%, alpha {row['alpha_max_rel_err']:.1e}, beta "
+          f"{row['beta_max_rel_err']:.1e}, err {row['final_error_gpu']:.6e} vs {row['final_error_ref']:.6e} "
+          f"[{kind}, {threads} threads: {t_cpu:.1f} s; GPU incl. PCIe {t_gpu:.2f} s] {'OK' if ok else 'FAIL'}",
+          flush=True)
+    del a, r, g, rel
+if "--json" in sys.argv:
+    json.dump(rows, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
+sys.exit(0 if all(r["within_1e-5"] for r in rows) else 1)
