@@ -9,6 +9,7 @@ tests enforce the 1e-5 bar and report the bitwise match.
 from __future__ import annotations
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -352,3 +353,17 @@ def test_rows_wider_than_the_grid_run_two_pass(gpu, orc, m, n, dt):
     rel = np.max(np.abs(plan.astype(np.float64) - ref.plan) / ref.plan)
     assert rel <= (1e-12 if dt == np.float64 else 1e-5), rel
     assert abs(err - ref.final_error) <= 1e-9 * max(1.0, ref.final_error)
+
+
+def test_baseline_config2_full_size_bitwise_vs_reference(gpu, ref):
+    # BASELINE config 2 at its full size and iteration count (8192^2, K=500) against the
+    # reference's own fused_solve (oracle/_ref, all host threads): identical plans
+    # (tools/full_parity.py runs configs 3 and 4 too: profiles/r01_full_parity.json)
+    import oracle
+    uot = gpu
+    a, rpd, cpd = oracle.Oracle().gen_problem(42, 8192, 8192, threads=os.cpu_count() or 1)
+    r = ref.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, 500, os.cpu_count() or 1)
+    g = uot.fused_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KNEVER, 500)
+    assert g.report.iterations == r.iterations == 500
+    assert np.array_equal(g.plan, r.plan)
+    np.testing.assert_allclose(g.factors.beta, r.beta, rtol=1e-12)
