@@ -31,6 +31,7 @@
 #include <cstring>
 #include <filesystem>
 #include <functional>
+#include <memory>
 #include <span>
 #include <string>
 #include <type_traits>
@@ -157,6 +158,13 @@ class Session {
     check(uot_get_plan(ctx_, m.data().data()));
     return m;
   }
+  // The plan into an existing rows() x cols() matrix (no reallocation).
+  void plan_into(Matrix<float>& m) const { check(uot_get_plan(ctx_, m.data().data())); }
+  // set_problem from the pieces, without assembling a Problem (no host copy of a).
+  void set_problem(const Matrix<float>& a, const std::vector<double>& rpd, const std::vector<double>& cpd,
+                   double er, double ep) {
+    check(uot_set_problem(ctx_, a.data().data(), rpd.data(), cpd.data(), er, ep));
+  }
   CommStats comm() const {
     CommStats c;
     std::uint64_t calls = 0, dbl = 0;
@@ -202,6 +210,15 @@ inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t m
   return r;
 }
 
+// fused_solve(p, tol, max_iter, std::size_t workers) (fused.hpp:287-291): the
+// worker count is a host-thread knob with no GPU meaning (results match any W to
+// the parity bar); the device is 0 — use the int overload above to pick one.
+template <typename T>
+inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t max_iter, std::size_t workers) {
+  if (workers < 1) throw InvalidParameter("fused_solve: workers must be at least 1");
+  return uot::cuda::fused_solve<T>(p, tol, max_iter, 0);
+}
+
 // fused_solve(p, tol, max_iter, const WorkerPlan&) (fused.hpp:259-285): the
 // reference's host worker plan has no GPU meaning — the sweep's CTA schedule
 // replaces it — but it is validated like the reference validates it, so a call
@@ -212,7 +229,7 @@ inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t m
                                   int device = 0) {
   if (plan.blocks.empty() || plan.blocks.back().end != p.m())
     throw InvalidParameter("fused_solve: plan does not cover the matrix rows");
-  return fused_solve(p, tol, max_iter, device);
+  return uot::cuda::fused_solve<T>(p, tol, max_iter, device);
 }
 
 namespace detail {
@@ -279,18 +296,22 @@ inline ScalingFactors fused_iterate(Matrix<float>& a, FusedState& state, const P
     throw InvalidParameter("fused_iterate: matrix shape does not match problem");
   if (state.col_sums.size() != a.cols())
     throw InvalidParameter("fused_iterate: carried column sums have wrong length");
-  Session s(a.rows(), a.cols(), device);
-  Problem<float> cur;
-  cur.a = a;
-  cur.rpd = p.rpd;
-  cur.cpd = p.cpd;
-  cur.er = p.er;
-  cur.ep = p.ep;
-  s.set_problem(cur);
+  // One device session per thread and shape, kept between calls: a loop over
+  // fused_iterate pays the two PCIe transfers per call, not a session setup.
+  thread_local std::unique_ptr<Session> cached;
+  thread_local std::size_t cr = 0, cc = 0;
+  thread_local int cd = -1;
+  if (!cached || cr != a.rows() || cc != a.cols() || cd != device) {
+    cached.reset();
+    cached = std::make_unique<Session>(a.rows(), a.cols(), device);
+    cr = a.rows(), cc = a.cols(), cd = device;
+  }
+  Session& s = *cached;
+  s.set_problem(a, p.rpd, p.cpd, p.er, p.ep);
   s.set_fi(fi);
   s.set_state(state);
   s.iterate(1);
-  a = s.plan();
+  s.plan_into(a);
   state = s.state();
   return s.factors();
 }
@@ -308,12 +329,12 @@ inline ScalingFactors fused_iterate_parallel(Matrix<float>& a, FusedState& state
     throw InvalidParameter("fused_iterate_parallel: plan does not cover the matrix rows");
   if (partials.workers() < plan.workers || partials.cols() != a.cols())
     throw InvalidParameter("fused_iterate_parallel: partial table does not fit the plan");
-  return fused_iterate(a, state, p, fi, device);
+  return uot::cuda::fused_iterate(a, state, p, fi, device);
 }
 inline ScalingFactors fused_iterate_parallel(Matrix<float>& a, FusedState& state, const Problem<float>& p,
                                              double fi, const WorkerPlan& plan, int device = 0) {
   PartialTable partials(plan.workers, a.cols());
-  return fused_iterate_parallel(a, state, p, fi, plan, partials, device);
+  return uot::cuda::fused_iterate_parallel(a, state, p, fi, plan, partials, device);
 }
 
 // distributed_solve (distributed.hpp:52-130) for rank `rank` of `nranks`
@@ -394,8 +415,11 @@ inline DistributedResult<float> distributed_solve_peer(const Problem<float>& p, 
 // (uot_create_group), rank r on GPU r mod (visible GPUs), one fused peer-memory
 // exchange of the column sums per iteration; the whole plan and alpha come back,
 // as in the reference. Blocks must be contiguous and non-empty.
-inline DistributedResult<float> distributed_solve(const Problem<float>& p, double tol, std::size_t max_iter,
-                                                  const RankPartition& part) {
+template <typename T>
+inline DistributedResult<T> distributed_solve(const Problem<T>& p, double tol, std::size_t max_iter,
+                                              const RankPartition& part) {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "Problem<float> or Problem<double>");
+  constexpr bool kF64 = std::is_same_v<T, double>;
   require_valid(p);
   if (!(tol > 0.0)) throw InvalidParameter("distributed_solve: tol must be positive");
   if (max_iter < 1) throw InvalidParameter("distributed_solve: max_iter must be at least 1");
@@ -421,24 +445,32 @@ inline DistributedResult<float> distributed_solve(const Problem<float>& p, doubl
       if (x && *uot_last_error(x)) msg = uot_last_error(x);
     raise(rc, msg);
   };
-  int rc = uot_create_group(ctx.data(), m, n, UOT_F32, nullptr, static_cast<int>(R), bounds.data());
+  int rc = uot_create_group(ctx.data(), m, n, kF64 ? UOT_F64 : UOT_F32, nullptr, static_cast<int>(R), bounds.data());
   if (rc) fail(rc);
   for (std::size_t r = 0; r < R; ++r) {
     const std::size_t b = bounds[r];
-    if ((rc = uot_set_problem(ctx[r], p.a.row(b), p.rpd.data() + b, p.cpd.data(), p.er, p.ep))) fail(rc);
+    if constexpr (kF64)
+      rc = uot_set_problem_f64(ctx[r], p.a.row(b), p.rpd.data() + b, p.cpd.data(), p.er, p.ep);
+    else
+      rc = uot_set_problem(ctx[r], p.a.row(b), p.rpd.data() + b, p.cpd.data(), p.er, p.ep);
+    if (rc) fail(rc);
   }
   if ((rc = uot_group_init_col_sums(ctx.data(), static_cast<int>(R)))) fail(rc);
   std::uint64_t it = 0;
   double err = 0.0;
   int conv = 0;
   if ((rc = uot_group_iterate(ctx.data(), static_cast<int>(R), max_iter, tol, &it, &err, &conv))) fail(rc);
-  DistributedResult<float> out;
-  out.plan = Matrix<float>(m, n);
+  DistributedResult<T> out;
+  out.plan = Matrix<T>(m, n);
   out.factors.alpha.resize(m);
   out.factors.beta.resize(n);
   for (std::size_t r = 0; r < R; ++r) {
     const std::size_t b = bounds[r];
-    if ((rc = uot_get_plan(ctx[r], out.plan.row(b)))) fail(rc);
+    if constexpr (kF64)
+      rc = uot_get_plan_f64(ctx[r], out.plan.row(b));
+    else
+      rc = uot_get_plan(ctx[r], out.plan.row(b));
+    if (rc) fail(rc);
     if ((rc = uot_get_factors(ctx[r], out.factors.alpha.data() + b, r == 0 ? out.factors.beta.data() : nullptr)))
       fail(rc);
   }
@@ -451,9 +483,10 @@ inline DistributedResult<float> distributed_solve(const Problem<float>& p, doubl
   out.report.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return out;
 }
-inline DistributedResult<float> distributed_solve(const Problem<float>& p, double tol, std::size_t max_iter,
-                                                  std::size_t ranks) {
-  return distributed_solve(p, tol, max_iter, RankPartition::make(ranks, p.m()));
+template <typename T>
+inline DistributedResult<T> distributed_solve(const Problem<T>& p, double tol, std::size_t max_iter,
+                                              std::size_t ranks) {
+  return uot::cuda::distributed_solve<T>(p, tol, max_iter, RankPartition::make(ranks, p.m()));
 }
 
 }  // namespace uot::cuda

@@ -405,9 +405,15 @@ int plan_layout(uot_ctx* ctx) {
   int smem_optin = 0;
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   // the TMEM-lag kernel's rings + factor rings must fit next to each other
-  ctx->dyn = env_int("UOT_DYNAMIC", 1) != 0;
   ctx->use_tmem = !f64 && env_int("UOT_TMEM", 0) != 0 && ctx->smem_tm <= static_cast<size_t>(smem_optin);
   ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * ctx->esz > (64ull << 20) ? 1 : 0;
+  // Dynamic batch schedule where per-SM bandwidth skew matters (streams past
+  // L2); smaller problems keep fixed row blocks: bit-reproducible run to run,
+  // like the reference's ordered reduction (UOT_DYNAMIC=0/1 forces either).
+  {
+    const int d = env_int("UOT_DYNAMIC", -1);
+    ctx->dyn = d < 0 ? ctx->evict_first : (d != 0);
+  }
   ctx->full = slice == epc * cfg->nt * cfg->v ? 1 : 0;
   int rc = probe_smid_map(ctx);
   if (rc) return rc;

@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -722,17 +723,27 @@ def fused_iterate(a: np.ndarray, state: FusedState, p: Problem, fi: float, devic
         _raise(1, "fused_iterate: matrix shape does not match problem")
     if np.asarray(state.col_sums).size != p.n():
         _raise(1, "fused_iterate: carried column sums have wrong length")
-    own = session is None
-    s = Session(p.m(), p.n(), device) if own else session
-    try:
-        s.set_problem(Problem(a, p.rpd, p.cpd, p.er, p.ep))
-        s.set_fi(fi)  # the caller's exponent, bit for bit
-        s.set_col_sums(state.col_sums)
-        s.iterate(1, 1e-300)
-        f = s.factors()
-        s.plan(out=a) if a.flags.c_contiguous and a.dtype == np.float32 else a.__setitem__(Ellipsis, s.plan())
-        state.col_sums = s.col_sums()
-    finally:
-        if own:
-            s.close()
+    s = session if session is not None else _cached_session(p.m(), p.n(), device)
+    s.set_problem(Problem(a, p.rpd, p.cpd, p.er, p.ep))
+    s.set_fi(fi)  # the caller's exponent, bit for bit
+    s.set_col_sums(state.col_sums)
+    s.iterate(1, 1e-300)
+    f = s.factors()
+    s.plan(out=a) if a.flags.c_contiguous and a.dtype == np.float32 else a.__setitem__(Ellipsis, s.plan())
+    state.col_sums = s.col_sums()
     return f
+
+
+_tls = threading.local()
+
+
+def _cached_session(m: int, n: int, device: int) -> "Session":
+    """One fp32 session per thread and (shape, device), kept between fused_iterate
+    calls: a loop pays the two PCIe transfers per call, not a session setup."""
+    key = (int(m), int(n), int(device))
+    s = getattr(_tls, "session", None)
+    if s is None or getattr(_tls, "key", None) != key or not s._h:
+        if s is not None:
+            s.close()
+        _tls.session, _tls.key = Session(m, n, device), key
+    return _tls.session
