@@ -11,7 +11,7 @@ BENCH_DEVICE=0 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-pe
 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 3 -c 1 -o gpurun_out/prof32 python tools/prof_sweep.py 32768 32768 5 > gpurun_out/prof32.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 3 -c 1 -o gpurun_out/prof262 python tools/prof_sweep.py 262144 4096 5 > gpurun_out/prof262.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:finalize_kernel -s 6 -c 1 -o gpurun_out/proffin python tools/prof_sweep.py 32768 32768 5 > gpurun_out/proffin.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:finalize_kernel -s 3 -c 1 -o gpurun_out/proffin python tools/prof_sweep.py 32768 32768 5 > gpurun_out/proffin.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:resident_kernel -c 1 -o gpurun_out/profres python tools/prof_sweep.py 1024 1024 20 > gpurun_out/profres.log 2>&1
 timeout 300 python tools/power_study.py 5 torch_rmw_rand,f32_32768,f64_32768x16384,f32_262144x4096 > gpurun_out/power.txt 2>&1
 timeout 300 tools/microbench/stream_bench 10 > gpurun_out/stream.txt 2>&1
