@@ -367,3 +367,32 @@ def test_baseline_config2_full_size_bitwise_vs_reference(gpu, ref):
     assert g.report.iterations == r.iterations == 500
     assert np.array_equal(g.plan, r.plan)
     np.testing.assert_allclose(g.factors.beta, r.beta, rtol=1e-12)
+
+
+def test_concurrent_sessions_in_threads(gpu, orc):
+    # independent sessions on one GPU from several host threads (ctypes drops the GIL):
+    # their sweeps interleave on the device; G > 1 launches stay cooperative so the
+    # SM-id-addressed CTAs of each grid remain a permutation (the seed included)
+    import threading
+    uot = gpu
+    cases = [(40, 32768, 5, 1), (64, 16384, 6, 2), (300, 3000, 7, 3), (5000, 1000, 4, 4)]
+    out, errs = {}, []
+
+    def work(m, n, k, seed):
+        try:
+            a, rpd, cpd = orc.gen_problem(seed, m, n)
+            out[seed] = (uot.fused_solve(uot.Problem(a, rpd, cpd, 1.0, 0.1), KNEVER, k),
+                         orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 2))
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    for _ in range(2):
+        ts = [threading.Thread(target=work, args=c) for c in cases]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert not errs, errs
+        for seed, (g, r) in out.items():
+            rel = np.max(np.abs(g.plan.astype(np.float64) - r.plan) / r.plan)
+            assert rel <= 1e-5 and g.report.iterations == r.iterations, (seed, rel)
