@@ -108,3 +108,11 @@ def test_group_device_list_must_match_ranks(gpu):
     uot = gpu
     with pytest.raises(uot.InvalidParameter):
         uot.SessionGroup(100, 100, 3, devices=[0, 0])
+
+
+def test_group_rows_wider_than_the_grid_are_refused(gpu, orc):
+    # G > #SMs is served by the two-pass schedule on ONE rank; the ablation
+    # schedules have no cross-rank exchange, so a multi-rank group refuses it
+    uot = gpu
+    with pytest.raises(uot.ConfigError):
+        uot.SessionGroup(4, 148 * 8192 + 100, 2, devices=[0, 0])
