@@ -9,6 +9,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -258,6 +259,7 @@ struct uot_ctx {
   unsigned char** d_peers = nullptr;      // device copy of peer_ptrs
   bool connected = false;
   bool group_local = false;  // a rank of a single-process group (uot_create_group): direct peer pointers, no IPC
+  uint64_t group_id = 0;     // which uot_create_group call made this rank (collectives check it)
   cudaEvent_t xev = nullptr;  // group: stage 1 of the running exchange is enqueued (cross-rank stream order)
 
   // layout
@@ -1763,8 +1765,8 @@ int group_check(uot_ctx* const* ctxs, int n) {
   for (int r = 0; r < n; ++r) {
     uot_ctx* c = ctxs[r];
     if (!c) return UOT_INVALID_PARAMETER;
-    if (c->nranks != n || c->rank != r || (n > 1 && !c->group_local))
-      return c->fail(UOT_INVALID_PARAMETER, "not rank %d of a %d-rank session group", r, n);
+    if (c->nranks != n || c->rank != r || (n > 1 && !c->group_local) || c->group_id != ctxs[0]->group_id)
+      return c->fail(UOT_INVALID_PARAMETER, "not rank %d of the %d-rank session group of rank 0", r, n);
   }
   return UOT_OK;
 }
@@ -1832,8 +1834,11 @@ int uot_create_group(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dty
                             cudaGetErrorString(e));
       cudaGetLastError();  // (clear "already enabled")
     }
+  static std::atomic<uint64_t> next_group{1};
+  const uint64_t gid = next_group.fetch_add(1);
   for (int r = 0; r < nranks; ++r) {
     uot_ctx* c = out[r];
+    c->group_id = gid;
     CKC(c, cudaSetDevice(c->device));
     c->peer_ptrs.assign(nranks, nullptr);
     for (int q = 0; q < nranks; ++q) c->peer_ptrs[q] = out[q]->region;

@@ -116,3 +116,12 @@ def test_group_rows_wider_than_the_grid_are_refused(gpu, orc):
     uot = gpu
     with pytest.raises(uot.ConfigError):
         uot.SessionGroup(4, 148 * 8192 + 100, 2, devices=[0, 0])
+
+
+def test_group_collectives_reject_ranks_of_different_groups(gpu):
+    uot = gpu
+    with uot.SessionGroup(40, 300, 2, devices=[0, 0]) as g1, uot.SessionGroup(40, 300, 2, devices=[0, 0]) as g2:
+        import ctypes as C
+        mixed = (C.c_void_p * 2)(g1.ranks[0]._h.value, g2.ranks[1]._h.value)
+        rc = uot.lib().uot_group_init_col_sums(C.cast(mixed, C.c_void_p), 2)
+        assert rc == 1  # UOT_INVALID_PARAMETER, no hang on a peer that never publishes
