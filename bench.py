@@ -5,22 +5,32 @@
 
 One step = one fused UOT iteration (fused_iterate_parallel, reference
 include/uot/fused.hpp:197-250): one sm_100a sweep over the resident matrix plus
-the O(cols) finalize (and, for N > 1, one NCCL allreduce of the column sums).
+the O(cols) finalize (for N > 1 with the per-iteration exchange of the column
+sums, distributed.hpp:88-100, fused into the finalize over peer memory).
 
-Workload (BASELINE.json metric): 32768 x 32768 fp32 per GPU, gen_problem_t seed
-42, reg=0.1 reg_m=1.0 (fi = 1/1.1). N GPUs weak-scale: the global problem is
-(32768*N) x 32768 row-sharded by RankPartition (N=4 is BASELINE config 5,
-131072 x 32768). `value` counts 32768^2-equivalent iterations per second over
-the whole job, so value(N) = N * value(1) is perfect scaling.
+Workloads (BASELINE.json configs, gen_problem_t seed 42, reg=0.1 reg_m=1.0,
+fi = 1/1.1):
+  N = 1   config 3, 32768 x 32768 fp32 (the headline);
+  N > 1   config 5, 131072 x 32768 fp32 row-sharded by RankPartition
+          (plan.cpp:35-44) over the N GPUs — strong scaling; rank 0 also times
+          the same 131072 x 32768 problem on ONE GPU first, so the line carries
+          parallel_efficiency = T1 / (N * T_N) measured in the same run.
+`value` counts 32768^2-equivalent iterations per second over the whole job (a
+config-5 iteration is 4 of them), so value(N) / (N * value(1)) is the scaling
+efficiency the driver computes.
 
-Under torchrun each rank drives its LOCAL_RANK GPU; torch.distributed (gloo)
-carries only barriers, the NCCL id and the max-over-ranks of the timings.
+`python bench.py --gpus N` re-launches itself under torch.distributed.run (one
+process per GPU); under torchrun each rank drives its LOCAL_RANK GPU and
+torch.distributed (gloo) carries only barriers, the peer-memory handles and the
+max-over-ranks of the device timings.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,8 +43,10 @@ sys.path.insert(0, HERE)
 
 METRIC = "UOT iterations/s and HBM GB/s (% of ~8 TB/s) at 32768² fp32, 1/2/4/8 B200"
 UNIT = "iterations/s (32768x32768 fp32-equivalent)"
-ROWS_PER_GPU = 32768
 COLS = 32768
+HEADLINE_ROWS = 32768      # config 3 (N = 1)
+SHARDED_ROWS = 131072      # config 5 (N > 1)
+UNIT_ELEMS = 32768 * 32768
 SEED = 42
 ER, EP = 1.0, 0.1  # reg_m = 1.0, reg = 0.1  ->  fi = 1/1.1
 KNEVER = 1e-300    # positive but unreachable: fixed-length runs (acceptance.cpp:26)
@@ -45,17 +57,26 @@ def env_int(name, default):
     return int(v) if v not in (None, "") else default
 
 
+def workload(world: int, rows_override: int = 0):
+    if rows_override:  # CPU tests only: a small stand-in, never a bench value
+        return rows_override, f"{rows_override}x32768 fp32 (--rows override: NOT a BASELINE config)"
+    rows = HEADLINE_ROWS if world == 1 else SHARDED_ROWS
+    name = ("config 3: 32768x32768 fp32" if world == 1 else
+            f"config 5: 131072x32768 fp32 row-sharded over {world} GPUs (RankPartition, plan.cpp:35-44)")
+    return rows, name
+
+
 # --------------------------------------------------------------- plumbing --
 
 class Group:
     """rank / world / barrier / max-reduce over the torchrun job (gloo), or a no-op."""
 
-    def __init__(self):
+    def __init__(self, init: bool = True):
         self.world = env_int("WORLD_SIZE", 1)
         self.rank = env_int("RANK", 0)
         self.local_rank = env_int("LOCAL_RANK", self.rank)
         self.dist = None
-        if self.world > 1:
+        if self.world > 1 and init:
             import torch.distributed as dist
             dist.init_process_group("gloo")
             self.dist = dist
@@ -72,6 +93,13 @@ class Group:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def gather(self, obj):
+        if not self.dist:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
     def close(self):
         if self.dist:
             self.dist.barrier()
@@ -79,23 +107,24 @@ class Group:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks, power and throttle reasons sampled during a timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_ms: int = 100):
         self.gpu = gpu
+        self.period_ms = period_ms
         self.proc = None
-        self.path = os.path.join(HERE, "gpurun_out", f".clocks_{os.getpid()}.csv")
+        self.path = os.path.join(HERE, "gpurun_out", f".clocks_{os.getpid()}_{gpu}.csv")
 
     def start(self):
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
             time.sleep(0.3)
         except (OSError, ValueError):
@@ -131,7 +160,8 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "samples": len(sm),
-                "power_w_max": max(power) if power else None, "reasons": sorted(reasons)}
+                "power_w_max": max(power) if power else None,
+                "power_w_median": statistics.median(power) if power else None, "reasons": sorted(reasons)}
 
 
 def peak_hbm():
@@ -145,7 +175,7 @@ def peak_hbm():
 
 def ncu_traffic(key: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per sweep launch from the
-    committed ncu --set full summary (profiles/ncu_traffic.json), or None."""
+    committed ncu --set full capture summary (profiles/ncu_traffic.json), or None."""
     try:
         with open(os.path.join(HERE, "profiles", "ncu_traffic.json")) as f:
             return json.load(f).get(key)
@@ -153,82 +183,115 @@ def ncu_traffic(key: str):
         return None
 
 
-# ------------------------------------------------------------- CPU arms --
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-def cpu_reference(steps: int, warmup: int, sample_rows: int, kind_pref: str = "reference"):
-    """Time the reference's fused_iterate_parallel (oracle/_ref: the unmodified
-    reference compiled from its sources; else the C restatement) with every host
-    thread on a row sample of the workload. Returns per-iteration ms list."""
+
+# ------------------------------------------------------------- CPU legs --
+
+def cpu_reference(rows: int, steps: int, warmup: int, w1_iters: int = 2):
+    """The reference's fused_iterate_parallel (oracle/_ref: the unmodified
+    reference compiled from its sources; else the C restatement) on the FULL
+    rows x COLS workload with every host thread (W = nproc), `warmup` untimed
+    then `steps` timed iterations; plus W = 1 on `w1_iters` iterations.
+    Generation and init_col_sums are excluded."""
     import oracle  # test/benchmark infrastructure only: the CPU baseline leg
     threads = os.cpu_count() or 1
-    kind = "port"
-    eng = None
-    if kind_pref == "reference":
-        try:
-            eng = oracle.RefOracle()
-            kind = "reference"
-        except (OSError, FileNotFoundError):
-            eng = None
-    if eng is None:
-        eng = oracle.Oracle()
     o = oracle.Oracle()
-    a, rpd, cpd = o.gen_problem(SEED, sample_rows, COLS, threads=threads)
-    if kind == "reference":
-        ms = eng.time_fused_iterate(a, rpd, cpd, ER, EP, threads, warmup + steps)
-    else:
-        cs = o.init_col_sums(a, threads)
+    try:
+        eng, kind = oracle.RefOracle(), "reference"
+    except (OSError, FileNotFoundError):
+        eng, kind = None, "port"
+    a, rpd, cpd = o.gen_problem(SEED, rows, COLS, threads=threads)
+
+    def timed(workers, k):
+        if eng is not None:
+            return list(eng.time_fused_iterate(a, rpd, cpd, ER, EP, workers, k))
+        cs = o.init_col_sums(a, workers)
         fi = o.compute_fi(ER, EP)
-        ms = []
-        for _ in range(warmup + steps):
+        out = []
+        for _ in range(k):
             t0 = time.perf_counter()
-            o.fused_iterate(a, cs, rpd, cpd, fi, threads)
-            ms.append((time.perf_counter() - t0) * 1e3)
-    ms = list(ms[warmup:]) or list(ms)
+            o.fused_iterate(a, cs, rpd, cpd, fi, workers)
+            out.append((time.perf_counter() - t0) * 1e3)
+        return out
+
+    ms = timed(threads, warmup + steps)[warmup:]
     mean_ms = sum(ms) / len(ms)
-    scale = (sample_rows * COLS) / (ROWS_PER_GPU * COLS)
-    value = scale * 1e3 / mean_ms
+    units = rows * COLS / UNIT_ELEMS
+    w1 = None
+    if w1_iters > 0:
+        ms1 = timed(1, w1_iters)
+        m1 = sum(ms1) / len(ms1)
+        w1 = {"workers": 1, "iterations": len(ms1), "ms_per_iter": m1, "value": units * 1e3 / m1,
+              "model_gbs": 2 * rows * COLS * 4 / m1 / 1e6}
     return {
-        "value": value, "unit": UNIT, "cores": threads, "kind": kind,
-        "sample": (f"rows 0..{sample_rows - 1} of gen_problem_t<float>(42, {sample_rows}, {COLS}); "
-                   f"fused_iterate_parallel W={threads}, {len(ms)} timed iterations after {warmup} warm-up "
-                   f"(mean {mean_ms:.1f} ms/iter, model {2 * sample_rows * COLS * 4 / mean_ms / 1e6:.1f} GB/s), "
-                   f"scaled by rows to {ROWS_PER_GPU}x{COLS}"),
-        "ms_per_iter": mean_ms,
+        "value": units * 1e3 / mean_ms, "unit": UNIT, "cores": threads, "kind": kind,
+        "sample": (f"full {rows}x{COLS} gen_problem_t<float>(42) workload; fused_iterate_parallel W={threads} "
+                   f"(all host threads), {len(ms)} timed iterations after {warmup} warm-up: mean {mean_ms:.1f} ms/iter, "
+                   f"model {2 * rows * COLS * 4 / mean_ms / 1e6:.1f} GB/s"),
+        "ms_per_iter": mean_ms, "iterations": len(ms), "warmup": warmup,
+        "cpu_model": cpu_model(), "w1": w1, "same_config": True,
     }
 
 
-def run_reference_arm(args, grp: Group):
-    if grp.rank != 0:
-        return None
-    sample_rows = args.cpu_sample_rows
-    cb = cpu_reference(args.steps, args.warmup, sample_rows, "reference")
+def run_reference_arm(args, world: int):
+    rows, name = workload(world, args.rows)
+    cb = cpu_reference(rows, args.steps, args.warmup, w1_iters=args.cpu_w1_iters if world == 1 else 1)
+    units = rows * COLS / UNIT_ELEMS
     return {
         "metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": cb["ms_per_iter"] / ((sample_rows * COLS) / (ROWS_PER_GPU * COLS)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "n_gpus": world, "steps": cb["iterations"], "warmup": cb["warmup"],
+        "ms_per_step": cb["ms_per_iter"] / units,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (gen_problem_t SplitMix64 seed 42), host memory",
-        "config": {"workload": f"{ROWS_PER_GPU}x{COLS} fp32 per GPU, fi=1/1.1 (reg=0.1, reg_m=1.0)",
-                   "rows": ROWS_PER_GPU, "cols": COLS, "parallelism": "cpu threads",
-                   "sample_rows": sample_rows},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "config": {"workload": f"{name}, reg=0.1 reg_m=1.0 (fi=1/1.1)", "rows": rows, "cols": COLS,
+                   "parallelism": f"cpu threads (W={cb['cores']}, {cb['cpu_model']})", "same_config": True},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "w1")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
 # --------------------------------------------------------------- our arm --
 
+def single_gpu_t1(rows: int, steps: int, warmup: int, dev: int) -> float:
+    """Device ms of `steps` iterations of the whole rows x COLS problem on ONE GPU
+    (the T1 of the strong-scaling efficiency)."""
+    from paper_2412_11079_b200 import uot
+    with uot.Session(rows, COLS, dev) as s:
+        s.generate_problem(SEED, ER, EP)
+        s.init_col_sums()
+        s.iterate(warmup, KNEVER)
+        it, _, _, ms = s.iterate_timed(steps, KNEVER)
+    if it != steps:
+        raise RuntimeError(f"T1 run: {it} of {steps} iterations")
+    return ms
+
+
 def run_ours(args, grp: Group):
     from paper_2412_11079_b200 import distributed as D
     from paper_2412_11079_b200 import uot
 
     world, rank = grp.world, grp.rank
-    rows_global = ROWS_PER_GPU * world
-    units = (rows_global * COLS) / (ROWS_PER_GPU * COLS)  # 32768^2-equivalents per iteration
+    rows_global, wname = workload(world, args.rows)
+    units = rows_global * COLS / UNIT_ELEMS  # 32768^2-equivalents per iteration
     dev = int(os.environ.get("BENCH_DEVICE", grp.local_rank))  # BENCH_DEVICE: ranks sharing one GPU (smoke only)
 
+    t1_ms = None
+    if world > 1 and not args.no_t1:
+        if rank == 0:
+            t1_ms = single_gpu_t1(rows_global, args.steps, args.warmup, dev)
+        grp.barrier()
+
     s = D.make_session(rows_global, COLS, dev, args.exchange)  # collective (peer handles / NCCL id)
-    exchange = s.exchange  # "nccl" when the peer mappings could not be made (make_session falls back)
+    exchange = s.exchange if world > 1 else "none"
     lay = s.layout
     rows_local = s.rows
 
@@ -254,12 +317,31 @@ def run_ours(args, grp: Group):
     max_ms = grp.max(dev_ms)
     value = units * args.steps / (max_ms / 1e3)
     bytes_iter_local = 2.0 * rows_local * COLS * 4  # metrics.cpp:69-72 model, this GPU
-    hbm_gbs = world * bytes_iter_local * args.steps / (max_ms / 1e3) / 1e9
+    hbm_gbs = 2.0 * rows_global * COLS * 4 * args.steps / (max_ms / 1e3) / 1e9
+    sweep_avg_ms = sweep_ms / max(nsweeps, 1)
+    fin_avg_us = fin_ms / max(nsweeps, 1) * 1e3
+    per_rank = grp.gather({"rank": rank, "rows": rows_local, "device_ms": dev_ms, "sweep_us": sweep_avg_ms * 1e3,
+                           "exchange_finalize_us": fin_avg_us})
 
     peak, peak_src = peak_hbm()
-    sweep_avg_ms = sweep_ms / max(nsweeps, 1)
     achieved = bytes_iter_local / (sweep_avg_ms / 1e3) / 1e9
-    traffic = ncu_traffic(f"{rows_local}x{COLS}")
+
+    # ---- sustained: >= args.sustained_s of back-to-back iterations ---------
+    sustained = None
+    if args.sustained_s > 0:
+        ksus = max(args.steps, int(math.ceil(args.sustained_s / (max_ms / args.steps / 1e3))))
+        grp.barrier()
+        s.synchronize()
+        cs = ClockSampler(dev, 200)
+        cs.start()
+        it_s, _, _, ms_s = s.iterate_timed(ksus, KNEVER)
+        s.synchronize()
+        clk_s = cs.stop()
+        ms_s = grp.max(ms_s)
+        sustained = {"iterations": it_s, "seconds": ms_s / 1e3, "value": units * it_s / (ms_s / 1e3),
+                     "hbm_gbs": 2.0 * rows_global * COLS * 4 * it_s / (ms_s / 1e3) / 1e9,
+                     "frac_of_8tbs": 2.0 * rows_global * COLS * 4 * it_s / (ms_s / 1e3) / 1e9 / (8000.0 * world),
+                     "clocks": clk_s}
 
     # ---- end to end through the public API with host buffers ---------------
     e2e = None
@@ -270,23 +352,23 @@ def run_ours(args, grp: Group):
         out = uot.PinnedBuffer((rows_local, COLS), np.float32)
         grp.barrier()
         t0 = time.perf_counter()
-        res = D.distributed_solve(p, KNEVER, args.steps, session=s, global_rows=rows_global) \
-            if world > 1 else None
-        if world == 1:
+        if world > 1:
+            res = D.distributed_solve(p, KNEVER, args.steps, session=s, global_rows=rows_global)
+            it2 = res.report.iterations
+            out.array[...] = res.plan
+        else:
             s.set_problem(p)              # H2D of A, rpd, cpd + validation (problem.hpp:64-103)
             s.init_col_sums()
             it2, _, _ = s.iterate(args.steps, KNEVER)
-            f = s.factors()                # D2H alpha, beta
+            s.factors()                    # D2H alpha, beta
             s.plan(out=out.array)          # D2H plan
-        else:
-            it2 = res.report.iterations
-            out.array[...] = res.plan
-        wall = time.perf_counter() - t0
-        wall = grp.max(wall)
+        wall = grp.max(time.perf_counter() - t0)
         h2d = rows_local * COLS * 4 + rows_local * 8 + COLS * 8
         d2h = rows_local * COLS * 4 + rows_local * 8 + COLS * 8
         e2e = {"value": units * it2 / wall, "unit": UNIT,
                "h2d_bytes_per_step": h2d * world / args.steps, "d2h_bytes_per_step": d2h * world / args.steps,
+               "wall_ms": wall * 1e3,
+               "pcie_gbs_if_serial": (h2d + d2h) / max(wall - max_ms / 1e3, 1e-9) / 1e9,
                "what": (f"fused_solve through the C ABI from page-locked host buffers: upload + validate "
                         f"{rows_local}x{COLS} per rank, init_col_sums, {args.steps} iterations, download "
                         f"plan + factors; wall {wall * 1e3:.1f} ms (max over ranks); per-step bytes = run bytes / steps")}
@@ -295,28 +377,30 @@ def run_ours(args, grp: Group):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(args.cpu_steps, 1, args.cpu_sample_rows, "reference")
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cb = cpu_reference(rows_global, args.cpu_steps or args.steps, args.warmup, w1_iters=args.cpu_w1_iters)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "w1", "same_config")}
     s.close()
 
     if rank != 0:
         return None
-    xdesc = (", column sums exchanged once per iteration inside the finalize kernels over peer memory "
-             "(CUDA IPC, NVLink): cols+1 f64 pushed to every rank, ascending-rank sum") \
-        if exchange == "peer" else ", NCCL allreduce of cols+N f64 per iteration"
-    return {
+    xdesc = {"peer": ", column sums exchanged once per iteration inside the finalize kernels over peer memory "
+                     "(NVLink): cols+1 f64 pushed to every rank, ascending-rank sum",
+             "nccl": ", one NCCL allreduce of cols+N f64 per iteration", "none": ""}[exchange]
+    line = {
         "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: gen_problem_t<float> SplitMix64 seed 42 bits, generated in HBM (value) / on the host (e2e)",
         "config": {
-            "workload": f"{ROWS_PER_GPU}x{COLS} fp32 per GPU (global {rows_global}x{COLS}), reg=0.1 reg_m=1.0 "
-                        f"(fi=1/1.1), {args.steps} fused iterations",
+            "workload": f"{wname}, reg=0.1 reg_m=1.0 (fi=1/1.1), {args.steps} fused iterations",
             "rows_global": rows_global, "cols": COLS, "rows_per_gpu": rows_local, "storage": "f32",
             "arithmetic": "f64 products rounded once to f32, f64 sums (bit-compatible with the reference)",
-            "parallelism": f"row-sharded x{world}" + (xdesc if world > 1 else ""),
+            "parallelism": f"row-sharded x{world}" + xdesc,
+            "schedule": "fixed row blocks (deterministic, bit-reproducible run to run)" if not lay["dynamic"]
+                        else "dynamic row batches",
             "l2": f"no flush: the resident matrix ({bytes_iter_local / 2 / 2**30:.1f} GiB/GPU) exceeds the 126 MB L2",
-            "layout": {k: lay[k] for k in ("G", "groups", "slice", "threads", "nbuf", "rows_per_step", "smem_bytes")},
+            "layout": {k: lay[k] for k in ("G", "groups", "slice", "threads", "nbuf", "rows_per_step", "smem_bytes",
+                                           "dynamic")},
         },
         "hbm_gbs": hbm_gbs,
         # the metric's own yardstick (report both): nominal 8 TB/s per GPU, and the measured copy peak
@@ -324,15 +408,45 @@ def run_ours(args, grp: Group):
         "hbm_frac_of_measured_copy": hbm_gbs / (peak * world),
         "final_error": err,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": ncu_traffic(f"{rows_local}x{COLS}"),
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + "
+                                       "dram__bytes_write.sum of one sweep launch of this shape)",
+                     "peak_source": peak_src,
                      "kernel": "uotk::sweep_kernel (fused row pass)",
                      "bytes_per_launch": bytes_iter_local, "avg_launch_ms": sweep_avg_ms,
-                     "finalize_avg_us": fin_ms / max(nsweeps, 1) * 1e3},
+                     "finalize_avg_us": fin_avg_us},
+        "sustained": sustained,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": gpu_launches,
         "clocks": clk,
     }
+    if world > 1:
+        sw = [r["sweep_us"] for r in per_rank]
+        line["per_rank"] = per_rank
+        line["rank_skew_us"] = max(sw) - min(sw)
+        line["exchange_finalize_us_max"] = max(r["exchange_finalize_us"] for r in per_rank)
+        if t1_ms is not None:
+            line["t1_ms_per_step"] = t1_ms / args.steps
+            line["parallel_efficiency"] = t1_ms / (world * max_ms)
+    return line
+
+
+# ------------------------------------------------------------- launcher --
+
+def free_port() -> int:
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: one process per GPU via
+    torch.distributed.run on this node (127.0.0.1 rendezvous)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -345,25 +459,37 @@ def main():
                     help="N>1: fused peer-memory exchange (default) or one NCCL allreduce per iteration")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-rows", type=int, default=8192)
-    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--no-t1", action="store_true", help="N>1: skip the single-GPU T1 run (no parallel_efficiency)")
+    ap.add_argument("--cpu-steps", type=int, default=0, help="cpu_baseline timed iterations (default: --steps)")
+    ap.add_argument("--cpu-w1-iters", type=int, default=2, help="cpu_baseline W=1 iterations (0: skip)")
+    ap.add_argument("--rows", type=int, default=0, help=argparse.SUPPRESS)  # tests: small stand-in workload
+    ap.add_argument("--sustained-s", type=float, default=2.0,
+                    help="seconds of back-to-back iterations for the `sustained` block (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    grp = Group()
-    if grp.world != args.gpus and grp.world > 1:
-        sys.stderr.write(f"note: --gpus {args.gpus} but WORLD_SIZE={grp.world}; using the launcher's world\n")
-    args.gpus = grp.world if grp.world > 1 else args.gpus
-    if args.gpus > 1 and grp.world == 1:
-        ap.error("N > 1 runs under torchrun (one process per GPU)")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    launched = "WORLD_SIZE" in os.environ
+    world = env_int("WORLD_SIZE", 1)
+    if launched and world > 1 and world != args.gpus:
+        sys.stderr.write(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using the launcher's world\n")
     if args.impl == "reference":
-        line = run_reference_arm(args, grp)
-    else:
-        line = run_ours(args, grp)
+        # the reference's CPU path on rank 0 only; other ranks exit without work
+        world = world if launched else args.gpus
+        if env_int("RANK", 0) != 0:
+            return 0
+        print(json.dumps(run_reference_arm(args, world)), flush=True)
+        return 0
+    if not launched and args.gpus > 1:
+        return relaunch_under_torchrun(args.gpus)
+    grp = Group()
+    line = run_ours(args, grp)
     grp.close()
     if line is not None:
         print(json.dumps(line), flush=True)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -7,7 +7,7 @@
 // DegenerateSum, PartitionError, ConfigError), so a reference user switches a
 // call site by changing the namespace:
 //
-//   uot::fused_solve(p, tol, max_iter, workers)   ->  uot::cuda::fused_solve(p, tol, max_iter)
+//   uot::fused_solve(p, tol, max_iter[, workers]) ->  uot::cuda::fused_solve(p, tol, max_iter[, workers])
 //   uot::fused_solve(p, tol, max_iter, plan)      ->  uot::cuda::fused_solve(p, tol, max_iter, plan)
 //   uot::fused_iterate(a, state, p, fi)           ->  uot::cuda::fused_iterate(a, state, p, fi)
 //   uot::fused_iterate_parallel(a, st, p, fi, plan[, partials]) -> uot::cuda::fused_iterate_parallel(same)
@@ -18,6 +18,10 @@
 //   uot::baseline_solve(p, tol, max_iter)         ->  uot::cuda::baseline_solve(p, tol, max_iter)
 //   uot::tiled_solve(p, tol, max_iter, ...)       ->  uot::cuda::tiled_solve(p, tol, max_iter)
 //   uot::read_problem(path) + solve               ->  uot::cuda::load(path).iterate(...)
+//
+// An integral 4th argument of fused_solve means workers everywhere, as in the
+// reference (fused.hpp:287-291); the GPU is chosen with a trailing
+// uot::cuda::Device{n} (default: device 0), never by a bare integer.
 //
 // plus uot::cuda::Session for loops that should keep the matrix resident in HBM
 // (the reference's per-iteration API moves the whole matrix every call).
@@ -57,6 +61,14 @@ namespace uot::cuda {
     default: throw Error("cuda backend: " + what);
   }
 }
+
+// The GPU a solver call runs on. A distinct type so that an integer argument in
+// a reference call site keeps its reference meaning (workers, ranks, ...).
+struct Device {
+  int id = 0;
+  constexpr Device() = default;
+  constexpr explicit Device(int i) : id(i) {}
+};
 
 // A problem resident on one B200 (or one rank's row block of it).
 class Session {
@@ -160,6 +172,15 @@ class Session {
   }
   // The plan into an existing rows() x cols() matrix (no reallocation).
   void plan_into(Matrix<float>& m) const { check(uot_get_plan(ctx_, m.data().data())); }
+  void plan_into(Matrix<double>& m) const { check(uot_get_plan_f64(ctx_, m.data().data())); }
+  // fused_iterate's inputs as given (fused.hpp:164-191): the current plan, the
+  // marginals and fi, uploaded without require_valid's checks.
+  template <typename T>
+  void set_iterate_input(const Matrix<T>& a, const std::vector<double>& rpd, const std::vector<double>& cpd,
+                         double fi) {
+    check(uot_set_iterate_input(ctx_, a.data().data(), std::is_same_v<T, double> ? UOT_F64 : UOT_F32, rpd.data(),
+                                cpd.data(), fi));
+  }
   // set_problem from the pieces, without assembling a Problem (no host copy of a).
   void set_problem(const Matrix<float>& a, const std::vector<double>& rpd, const std::vector<double>& cpd,
                    double er, double ep) {
@@ -185,13 +206,13 @@ class Session {
 // Problem<double>. The plan, factors and report have the reference's meaning;
 // report.solver is "cuda" and wall_ms also covers the PCIe transfers.
 template <typename T>
-inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t max_iter, int device = 0) {
+inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t max_iter, Device device = Device{}) {
   static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "Problem<float> or Problem<double>");
   require_valid(p);
   if (!(tol > 0.0)) throw InvalidParameter("fused_solve: tol must be positive");
   if (max_iter < 1) throw InvalidParameter("fused_solve: max_iter must be at least 1");
   const auto t0 = std::chrono::steady_clock::now();
-  Session s(p.m(), p.n(), device, std::is_same_v<T, double> ? Dtype::f64 : Dtype::f32);
+  Session s(p.m(), p.n(), device.id, std::is_same_v<T, double> ? Dtype::f64 : Dtype::f32);
   s.set_problem(p);
   s.init_col_sums();
   const auto pr = s.iterate(max_iter, tol);
@@ -210,13 +231,16 @@ inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t m
   return r;
 }
 
-// fused_solve(p, tol, max_iter, std::size_t workers) (fused.hpp:287-291): the
-// worker count is a host-thread knob with no GPU meaning (results match any W to
-// the parity bar); the device is 0 — use the int overload above to pick one.
-template <typename T>
-inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t max_iter, std::size_t workers) {
-  if (workers < 1) throw InvalidParameter("fused_solve: workers must be at least 1");
-  return uot::cuda::fused_solve<T>(p, tol, max_iter, 0);
+// fused_solve(p, tol, max_iter, std::size_t workers) (fused.hpp:287-291). Any
+// integral 4th argument binds here and means workers, as in the reference
+// (uot::cuda::fused_solve(p, tol, 200, 8) is 8 workers, not GPU 8). The worker
+// count is a host-thread knob with no GPU meaning (results match any W to the
+// parity bar); it is validated like WorkerPlan::make validates it.
+template <typename T, typename W, std::enable_if_t<std::is_integral_v<W> && !std::is_same_v<W, bool>, int> = 0>
+inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t max_iter, W workers,
+                                  Device device = Device{}) {
+  if (workers < W(1)) throw InvalidParameter("fused_solve: workers must be at least 1");
+  return uot::cuda::fused_solve<T>(p, tol, max_iter, device);
 }
 
 // fused_solve(p, tol, max_iter, const WorkerPlan&) (fused.hpp:259-285): the
@@ -226,7 +250,7 @@ inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t m
 // parity bar (the reference's own W-independence, test_fused.cpp).
 template <typename T>
 inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t max_iter, const WorkerPlan& plan,
-                                  int device = 0) {
+                                  Device device = Device{}) {
   if (plan.blocks.empty() || plan.blocks.back().end != p.m())
     throw InvalidParameter("fused_solve: plan does not cover the matrix rows");
   return uot::cuda::fused_solve<T>(p, tol, max_iter, device);
@@ -234,14 +258,14 @@ inline SolveResult<T> fused_solve(const Problem<T>& p, double tol, std::size_t m
 
 namespace detail {
 template <typename T>
-inline SolveResult<T> solve_with(const Problem<T>& p, double tol, std::size_t max_iter, int device, int variant,
+inline SolveResult<T> solve_with(const Problem<T>& p, double tol, std::size_t max_iter, Device device, int variant,
                                  const char* solver, const char* who) {
   static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "Problem<float> or Problem<double>");
   require_valid(p);
   if (!(tol > 0.0)) throw InvalidParameter(std::string(who) + ": tol must be positive");
   if (max_iter < 1) throw InvalidParameter(std::string(who) + ": max_iter must be at least 1");
   const auto t0 = std::chrono::steady_clock::now();
-  Session s(p.m(), p.n(), device, std::is_same_v<T, double> ? Dtype::f64 : Dtype::f32);
+  Session s(p.m(), p.n(), device.id, std::is_same_v<T, double> ? Dtype::f64 : Dtype::f32);
   s.set_problem(p);
   s.init_col_sums();
   s.set_variant(variant);
@@ -265,50 +289,56 @@ inline SolveResult<T> solve_with(const Problem<T>& p, double tol, std::size_t ma
 // baseline_solve (baseline.hpp:118-142): the four-sweep schedule on the GPU
 // (an ablation of the fused sweep: 3x its HBM traffic).
 template <typename T>
-inline SolveResult<T> baseline_solve(const Problem<T>& p, double tol, std::size_t max_iter, int device = 0) {
+inline SolveResult<T> baseline_solve(const Problem<T>& p, double tol, std::size_t max_iter,
+                                     Device device = Device{}) {
   return detail::solve_with(p, tol, max_iter, device, UOT_VARIANT_BASELINE, "baseline", "baseline_solve");
 }
 
 // tiled_solve (tiled.hpp:231-260): the paper's two-pass GPU data flow (part4 ->
 // row factors -> part2); the reference's TileConfig shapes have no meaning here.
 template <typename T>
-inline SolveResult<T> tiled_solve(const Problem<T>& p, double tol, std::size_t max_iter, int device = 0) {
+inline SolveResult<T> tiled_solve(const Problem<T>& p, double tol, std::size_t max_iter, Device device = Device{}) {
   return detail::solve_with(p, tol, max_iter, device, UOT_VARIANT_TWO_PASS, "tiled", "tiled_solve");
 }
 
 // A session holding the problem of a .uotp file (read_problem, problem_io.cpp:106-141).
-inline Session load(const std::filesystem::path& path, int device = 0) {
+inline Session load(const std::filesystem::path& path, Device device = Device{}) {
   std::uint64_t m = 0, n = 0;
   int dtype = 0;
   double er = 0, ep = 0;
   const int rc = uot_problem_file_info(path.c_str(), &m, &n, &dtype, &er, &ep);
   if (rc != UOT_OK) raise(rc, uot_last_io_error());
-  Session s(m, n, device, dtype == UOT_F64 ? Dtype::f64 : Dtype::f32);
+  Session s(m, n, device.id, dtype == UOT_F64 ? Dtype::f64 : Dtype::f32);
   s.load_problem_file(path);
   return s;
 }
 
-// fused_iterate (fused.hpp:164-191): `a` and `state` updated in place. Moves
-// the matrix over PCIe twice per call; prefer Session for loops.
-inline ScalingFactors fused_iterate(Matrix<float>& a, FusedState& state, const Problem<float>& p,
-                                    double fi, int device = 0) {
+// fused_iterate (fused.hpp:164-191) for Problem<float> or Problem<double>: `a`
+// and `state` updated in place. Like the reference it takes fi and the plan as
+// given — no require_valid, no positivity check of the current plan — and
+// throws DegenerateSum where beta_from_state / rescale_factor would. Moves the
+// matrix over PCIe twice per call; prefer Session for loops.
+template <typename T>
+inline ScalingFactors fused_iterate(Matrix<T>& a, FusedState& state, const Problem<T>& p, double fi,
+                                    Device device = Device{}) {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "Matrix<float> or Matrix<double>");
   if (a.rows() != p.m() || a.cols() != p.n())
     throw InvalidParameter("fused_iterate: matrix shape does not match problem");
   if (state.col_sums.size() != a.cols())
     throw InvalidParameter("fused_iterate: carried column sums have wrong length");
-  // One device session per thread and shape, kept between calls: a loop over
-  // fused_iterate pays the two PCIe transfers per call, not a session setup.
+  // One device session per thread, shape and dtype, kept between calls: a loop
+  // over fused_iterate pays the two PCIe transfers per call, not a session setup.
   thread_local std::unique_ptr<Session> cached;
   thread_local std::size_t cr = 0, cc = 0;
   thread_local int cd = -1;
-  if (!cached || cr != a.rows() || cc != a.cols() || cd != device) {
+  if (!cached || cr != a.rows() || cc != a.cols() || cd != device.id) {
     cached.reset();
-    cached = std::make_unique<Session>(a.rows(), a.cols(), device);
-    cr = a.rows(), cc = a.cols(), cd = device;
+    cached = std::make_unique<Session>(a.rows(), a.cols(), device.id,
+                                       std::is_same_v<T, double> ? Dtype::f64 : Dtype::f32);
+    cr = a.rows(), cc = a.cols(), cd = device.id;
   }
   Session& s = *cached;
-  s.set_problem(a, p.rpd, p.cpd, p.er, p.ep);
-  s.set_fi(fi);
+  s.set_iterate_input(a, p.rpd, p.cpd, fi);
   s.set_state(state);
   s.iterate(1);
   s.plan_into(a);
@@ -318,9 +348,10 @@ inline ScalingFactors fused_iterate(Matrix<float>& a, FusedState& state, const P
 
 // fused_iterate_parallel (fused.hpp:197-257) with the reference's checks on the
 // plan and partial table; the GPU does the iteration (fused_iterate above).
-inline ScalingFactors fused_iterate_parallel(Matrix<float>& a, FusedState& state, const Problem<float>& p,
-                                             double fi, const WorkerPlan& plan, PartialTable& partials,
-                                             int device = 0) {
+template <typename T>
+inline ScalingFactors fused_iterate_parallel(Matrix<T>& a, FusedState& state, const Problem<T>& p, double fi,
+                                             const WorkerPlan& plan, PartialTable& partials,
+                                             Device device = Device{}) {
   if (a.rows() != p.m() || a.cols() != p.n())
     throw InvalidParameter("fused_iterate_parallel: matrix shape does not match problem");
   if (state.col_sums.size() != a.cols())
@@ -329,12 +360,13 @@ inline ScalingFactors fused_iterate_parallel(Matrix<float>& a, FusedState& state
     throw InvalidParameter("fused_iterate_parallel: plan does not cover the matrix rows");
   if (partials.workers() < plan.workers || partials.cols() != a.cols())
     throw InvalidParameter("fused_iterate_parallel: partial table does not fit the plan");
-  return uot::cuda::fused_iterate(a, state, p, fi, device);
+  return uot::cuda::fused_iterate<T>(a, state, p, fi, device);
 }
-inline ScalingFactors fused_iterate_parallel(Matrix<float>& a, FusedState& state, const Problem<float>& p,
-                                             double fi, const WorkerPlan& plan, int device = 0) {
+template <typename T>
+inline ScalingFactors fused_iterate_parallel(Matrix<T>& a, FusedState& state, const Problem<T>& p, double fi,
+                                             const WorkerPlan& plan, Device device = Device{}) {
   PartialTable partials(plan.workers, a.cols());
-  return uot::cuda::fused_iterate_parallel(a, state, p, fi, plan, partials, device);
+  return uot::cuda::fused_iterate_parallel<T>(a, state, p, fi, plan, partials, device);
 }
 
 // distributed_solve (distributed.hpp:52-130) for rank `rank` of `nranks`

@@ -38,8 +38,8 @@ extern "C" {
 
 /* Dtype codes: uot::Dtype (include/uot/matrix.hpp:13). Both have a kernel: f32
  * storage with f64 arithmetic (the products rounded once to fp32, as T(double)
- * in fused.hpp:128-140), or f64 storage (plain f64 products). The resident,
- * TMEM, persistent and ablation paths are f32-only. */
+ * in fused.hpp:128-140), or f64 storage (plain f64 products). The resident
+ * (whole solve in one launch) path is f32-only. */
 #define UOT_F32 1
 #define UOT_F64 2
 
@@ -70,9 +70,7 @@ typedef struct uot_layout {
   int32_t rank, nranks, device, evict_first;
   int32_t smid_map;      /* sweep CTAs addressed by SM id (row groups on neighbouring SMs) */
   int32_t exchange;      /* 0 single GPU, 1 NCCL allreduce, 2 fused peer-memory exchange */
-  int32_t tmem;          /* iterations park the alpha-lag rows in Tensor Memory (sweep_tmem.cuh) */
   int32_t resident;      /* uot_iterate runs as ONE persistent launch, matrix in shared memory (resident.cuh) */
-  int32_t persist;       /* otherwise, single rank: ONE persistent streaming launch (persist.cuh) */
   int32_t dtype;         /* UOT_F32 (Problem<float>) or UOT_F64 (Problem<double>) */
   int32_t dynamic;       /* 1: row batches handed out by a device counter (uot_set_deterministic) */
   int32_t variant;       /* iteration schedule (UOT_VARIANT_*); rows wider than #SMs slices (G > #SMs,
@@ -157,13 +155,18 @@ UOT_API int uot_save_problem_file(uot_ctx* ctx, const char* path);
 #define UOT_VARIANT_BASELINE 2
 UOT_API int uot_set_variant(uot_ctx* ctx, int variant);
 
-/* Row-batch schedule of the fused sweep. Default (0): batches go to whichever
- * CTA asks next (a device counter), so SMs with more HBM bandwidth take more
- * rows; the f64 column sums then add rows in a run-dependent order (results
- * agree to ~1e-12 relative between runs). 1: every row group owns a fixed
- * contiguous row block (balanced_blocks, plan.cpp:11-21): bit-reproducible
- * run to run, slower where per-SM bandwidth differs. */
+/* Row-batch schedule of the fused sweep. Default (1): every row group owns a
+ * fixed contiguous row block (balanced_blocks, plan.cpp:11-21) and the column
+ * partials are reduced in ascending group order: bit-reproducible run to run,
+ * as the reference's ordered reduction (fused.hpp:193-196, 242-248). 0: batches
+ * go to whichever CTA asks next (a device counter), so SMs with more HBM
+ * bandwidth take more rows; the f64 column sums then add rows in a
+ * run-dependent order (results agree to ~1e-12 relative between runs). */
 UOT_API int uot_set_deterministic(uot_ctx* ctx, int on);
+/* Small single-GPU f32 problems whose row blocks fit shared memory run a whole
+ * uot_iterate call as ONE cooperative launch (resident.cuh). Default 1; 0 keeps
+ * the streaming sweep + finalize per iteration (tests, ablations). */
+UOT_API int uot_set_resident(uot_ctx* ctx, int on);
 
 UOT_API void uot_destroy(uot_ctx* ctx);
 UOT_API const char* uot_last_error(const uot_ctx* ctx);
@@ -188,6 +191,14 @@ UOT_API int uot_generate_problem(uot_ctx* ctx, uint64_t seed, double er, double 
 /* Override the damping exponent (fused_iterate takes fi directly, fused.hpp:165).
  * fi must lie in (0, 1]. */
 UOT_API int uot_set_fi(uot_ctx* ctx, double fi);
+/* fused_iterate's inputs as the caller holds them (fused.hpp:164-191): the
+ * current plan `a` (dtype UOT_F32 or UOT_F64, must match the session), rpd,
+ * cpd and fi, uploaded WITHOUT require_valid's checks — the reference's
+ * fused_iterate validates only shapes, and throws DegenerateSum from
+ * rescale_factor, which the device reports the same way. Resets the iteration
+ * state; follow with uot_set_col_sums (the FusedState) and uot_iterate(1). */
+UOT_API int uot_set_iterate_input(uot_ctx* ctx, const void* a, int dtype, const double* rpd, const double* cpd,
+                                  double fi);
 /* Replace only the plan (the current matrix) of this rank; marginals stay. */
 UOT_API int uot_set_plan(uot_ctx* ctx, const float* a);
 UOT_API int uot_set_plan_f64(uot_ctx* ctx, const double* a);

@@ -201,6 +201,8 @@ class RefOracle:
         L.ref_fused_iterate_k_f32.argtypes = [_P, _sz, _sz, _P, _P, _d, _d, _sz, _sz, _P, _P, _P,
                                               _P, C.POINTER(_d)]
         L.ref_time_fused_iterate_f32.argtypes = [_P, _sz, _sz, _P, _P, _d, _d, _sz, _sz, _P]
+        L.ref_fused_iterate_k_inplace_f32.argtypes = [_P, _sz, _sz, _P, _P, _d, _d, _sz, _sz, _P, _P, _P,
+                                                      C.POINTER(_d)]
         L.ref_distributed_solve_f32.argtypes = [
             _P, _sz, _sz, _P, _P, _d, _d, _d, _sz, _sz, _P, _P, _P,
             C.POINTER(_sz), C.POINTER(_d), C.POINTER(_i), C.POINTER(_u64), C.POINTER(_u64)]
@@ -286,6 +288,21 @@ class RefOracle:
                                                      workers, k, _ptr(plan), _ptr(alpha),
                                                      _ptr(beta), _ptr(cs), C.byref(err)))
         return SolveOut(plan, alpha, beta, k, err.value, False, cs)
+
+    def fused_iterate_k_inplace(self, a, rpd, cpd, er, ep, workers, k) -> SolveOut:
+        """fused_iterate_k with `a` (C-contiguous float32) overwritten by the
+        plan: two host copies of the matrix instead of four (config 5)."""
+        if a.dtype != np.float32 or not a.flags.c_contiguous:
+            raise ValueError("a must be a C-contiguous float32 array")
+        m, n = a.shape
+        alpha = np.empty(m, np.float64)
+        beta = np.empty(n, np.float64)
+        cs = np.empty(n, np.float64)
+        err = _d()
+        self._check(self.lib.ref_fused_iterate_k_inplace_f32(_ptr(a), m, n, _ptr(rpd), _ptr(cpd), er, ep,
+                                                             workers, k, _ptr(alpha), _ptr(beta), _ptr(cs),
+                                                             C.byref(err)))
+        return SolveOut(a, alpha, beta, k, err.value, False, cs)
 
     def time_fused_iterate(self, a, rpd, cpd, er, ep, workers, k):
         a = np.ascontiguousarray(a, np.float32)

@@ -157,22 +157,45 @@ int ref_fused_iterate_k_f32(const float* a, std::size_t m, std::size_t n, const 
 
 // Wall-clock timing of fused_iterate_parallel, seeding and problem setup
 // excluded. Returns per-iteration milliseconds in ms_per_iter[k].
+// The iteration runs on p.a itself (fused_iterate_parallel reads the Problem
+// only for its shape, rpd and cpd: fused.hpp:201-223), so a 16 GiB config-5
+// matrix costs one host copy, not two.
 int ref_time_fused_iterate_f32(const float* a, std::size_t m, std::size_t n, const double* rpd,
                                const double* cpd, double er, double ep, std::size_t workers,
                                std::size_t k, double* ms_per_iter) {
   return guarded([&] {
-    const auto p = make_problem(a, m, n, rpd, cpd, er, ep);
+    auto p = make_problem(a, m, n, rpd, cpd, er, ep);
     const double fi = uot::compute_fi(er, ep);
     const auto plan = uot::WorkerPlan::make(workers, m, n);
-    uot::Matrix<float> x = p.a;
-    uot::FusedState st{uot::init_col_sums(x, std::span<const uot::WorkerBlock>(plan.blocks))};
+    uot::FusedState st{uot::init_col_sums(p.a, std::span<const uot::WorkerBlock>(plan.blocks))};
     uot::PartialTable partials(plan.workers, n);
     for (std::size_t it = 0; it < k; ++it) {
       const auto t0 = std::chrono::steady_clock::now();
-      (void)uot::fused_iterate_parallel(x, st, p, fi, plan, partials);
+      (void)uot::fused_iterate_parallel(p.a, st, p, fi, plan, partials);
       ms_per_iter[it] =
           std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
+  });
+}
+
+// ref_fused_iterate_k_f32 for matrices too large for four host copies (config
+// 5: 16 GiB): the caller's buffer `a` receives the plan after k iterations
+// (one internal copy; the iteration runs on p.a, see above).
+int ref_fused_iterate_k_inplace_f32(float* a, std::size_t m, std::size_t n, const double* rpd,
+                                    const double* cpd, double er, double ep, std::size_t workers,
+                                    std::size_t k, double* alpha, double* beta, double* col_sums,
+                                    double* final_error) {
+  return guarded([&] {
+    auto p = make_problem(static_cast<const float*>(a), m, n, rpd, cpd, er, ep);
+    const double fi = uot::compute_fi(er, ep);
+    const auto plan = uot::WorkerPlan::make(workers, m, n);
+    uot::FusedState st{uot::init_col_sums(p.a, std::span<const uot::WorkerBlock>(plan.blocks))};
+    uot::PartialTable partials(plan.workers, n);
+    uot::ScalingFactors f;
+    for (std::size_t it = 0; it < k; ++it) f = uot::fused_iterate_parallel(p.a, st, p, fi, plan, partials);
+    copy_out(p.a, f, a, alpha, beta);
+    if (col_sums) std::memcpy(col_sums, st.col_sums.data(), n * sizeof(double));
+    if (final_error) *final_error = uot::convergence_error(f);
   });
 }
 

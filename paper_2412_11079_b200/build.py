@@ -25,7 +25,7 @@ def nvcc_cmd(out: str = SO, extra: list[str] | None = None) -> list[str]:
     return [
         NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
         "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-        "-Xptxas", "-v", "--expt-relaxed-constexpr",
+        "-Xptxas", "-v", "--expt-relaxed-constexpr", "--compress-mode=size",
         "-I", os.path.join(ROOT, "include"),
         *(extra or []), "-o", out, *SOURCES, "-ldl", "-lpthread",
     ]

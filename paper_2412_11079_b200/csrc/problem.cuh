@@ -96,6 +96,13 @@ __global__ void reset_control_kernel(Control* c) {
   c->batch_next = 0;
 }
 
+// A caller-supplied FusedState (uot_set_col_sums): a converged session may run
+// again; a failed one stays stopped.
+__global__ void resume_control_kernel(Control* c) {
+  c->converged = 0;
+  c->done = c->status != 0 ? 1 : 0;
+}
+
 // Start of an iterate() call: new tolerance; a failed session stays stopped.
 __global__ void begin_iterate_kernel(Control* c, double tol) {
   c->tol = tol;

@@ -256,12 +256,8 @@ __device__ __forceinline__ void group_sweep1(float4* row, float4 (&v)[KG], uint3
 
 // Sweep 2 of one chunk group (fused.hpp:135-142): x <- f32(f64(x)*alpha) in
 // place, next_j += f64(x). EXACT: x1 may be non-normal (hardware widening).
-// UOT_S2_FASTD: the column sums widen x2 with fastd after a screen of the
-// group (off the 16/clk/SM conversion pipe): +1.3% at 32768^2 (measured);
-// 0 = the hardware conversion for every value.
-#ifndef UOT_S2_FASTD
-#define UOT_S2_FASTD 1
-#endif
+// The column sums widen x2 with fastd after a screen of the group (off the
+// 16/clk/SM conversion pipe): +1.3% at 32768^2 over F2F.F64.F32 (measured).
 template <int NT, int KG, bool FULL, bool EXACT>
 __device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g0, unsigned tid, unsigned nq,
                                              double al, double* acc) {
@@ -270,7 +266,6 @@ __device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       comp(w[kk], e) = d2f((EXACT ? static_cast<double>(comp(w[kk], e)) : fastd(comp(w[kk], e))) * al);
-#if UOT_S2_FASTD
   // x2 screened positive normal: widen with integer ops (off the conversion pipe)
   uint32_t m = 0;
 #pragma unroll
@@ -278,13 +273,11 @@ __device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g
 #pragma unroll
     for (int e = 0; e < 4; ++e) m = nn_max(m, comp(w[kk], e));
   const bool ok = nn_ok(m);
-#endif
 #pragma unroll
   for (int kk = 0; kk < KG; ++kk) {
     const unsigned q = tid + (g0 + kk) * NT;
     if (FULL || q < nq) {
       row[q] = w[kk];
-#if UOT_S2_FASTD
       if (ok) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += fastd(comp(w[kk], e));
@@ -292,10 +285,6 @@ __device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(w[kk], e));
       }
-#else
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(w[kk], e));
-#endif
     }
   }
 }
@@ -493,26 +482,6 @@ __device__ __forceinline__ void row_seed_f64(const double2* row, unsigned tid, u
       const double2 v = row[q];
       acc[2 * k] += v.x;
       acc[2 * k + 1] += v.y;
-    }
-  }
-}
-
-// Experiment builds (-DUOT_EXP=1: the compute warps leave the ring untouched,
-// the pipeline alone; 2: they read and write every chunk back, no f64 math).
-#ifndef UOT_EXP
-#define UOT_EXP 0
-#endif
-template <int NT, int V>
-__device__ __forceinline__ void exp_touch(float4* row, unsigned tid) {
-  if (UOT_EXP == 2) {
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      float4 v = row[tid + k * NT];
-      v.x += 0.0f;
-      v.y += 0.0f;
-      v.z += 0.0f;
-      v.w += 0.0f;
-      row[tid + k * NT] = v;
     }
   }
 }
@@ -771,12 +740,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       TR_BEGIN();
       double al = 0.0;
       if (lane < static_cast<int>(nr)) {
-#if UOT_EXP
-        al = 1.0;  // experiment builds: the row sums are not computed
-        if (false) {
-#else
         if (!rescale_factor_dev(rv, t, a.fi, &al)) {
-#endif
           atomicOr(&ctl->alpha_bad, 1);
           al = 1.0;
         }
@@ -815,7 +779,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   // ========================================================= compute warps ==
   double beta[EPC * V], acc[EPC * V];
 #pragma unroll
-  for (int i = 0; i < EPC * V; ++i) acc[i] = UOT_EXP ? 1.0 : 0.0;  // (experiments: positive column sums)
+  for (int i = 0; i < EPC * V; ++i) acc[i] = 0.0;
   ScreenBounds sb{0xffffffffu, 0u};
   if (!SEED) {
     const double* bsrc = a.beta2 + ((ctl->iter + 1) & 1ull) * a.pitch + static_cast<size_t>(g) * a.slice;
@@ -889,9 +853,6 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
             if constexpr (F64) {
               part[r] = row_sweep1_f64<NT, V, FULL>(reinterpret_cast<double2*>(buf + r * a.slice), tid, nq, beta);
             } else {
-#if UOT_EXP
-              exp_touch<NT, V>(reinterpret_cast<float4*>(buf + r * a.slice), tid);
-#else
               bool bad = false;
               if constexpr (TB)
                 part[r] = row_sweep1_tb<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, tcol,
@@ -900,7 +861,6 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
                 part[r] =
                     row_sweep1<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq, beta, sb, bad);
               if (bad) x1bad |= static_cast<Mask>(1u) << (sh + r);
-#endif
             }
           }
         }
@@ -919,12 +879,8 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
               row_sweep2_f64<NT, V, FULL>(reinterpret_cast<double2*>(buf + r * a.slice), tid, nq,
                                           alpha_s[(b % kQ) * BM + r], acc);
             else
-#if UOT_EXP
-              exp_touch<NT, V>(reinterpret_cast<float4*>(buf + r * a.slice), tid);
-#else
               row_sweep2<NT, V, FULL>(reinterpret_cast<float4*>(buf + r * a.slice), tid, nq,
                                       alpha_s[(b % kQ) * BM + r], (x1bad >> (sh + r)) & 1u, acc);
-#endif
           }
         fence_proxy_async_smem();  // generic writes -> the producer's bulk store
         __syncwarp();

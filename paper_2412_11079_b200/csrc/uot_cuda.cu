@@ -23,10 +23,8 @@
 #include "finalize.cuh"
 #include "problem.cuh"
 #include "sweep.cuh"
-#include "sweep_tmem.cuh"
 #include "resident.cuh"
 #include "ablation.cuh"
-#include "persist.cuh"
 
 using namespace uotk;
 
@@ -40,59 +38,24 @@ using SweepFn = void (*)(const SweepArgs);
 struct SweepCfg {
   int nt, v, bm, nbuf, nf;
   bool xchg;           // rows span G > 1 CTAs (cross-CTA row-sum exchange)
-  SweepFn iter[2];     // [FULL] smem-ring iteration kernel (sweep.cuh)
-  SweepFn seed[2];     // [FULL]
-  SweepFn iter_tm[2];  // [FULL] TMEM-lag iteration kernel (sweep_tmem.cuh)
-  void (*persist[2])(const PersistArgs);  // [FULL] K iterations per launch (persist.cuh)
-  int la_tm;
+  SweepFn iter[2];     // [FULL] iteration kernel
+  SweepFn seed[2];     // [FULL] init_col_sums kernel
   size_t (*smem_bytes)(unsigned buf_stride);
-  size_t (*smem_bytes_tm)(unsigned buf_stride);
 };
 
-// Sweep 2 lags sweep 1 by LA = 2 extra batches (the factor warps' budget: the
-// pow and, for G > 1, the L2 exchange round trip). NF factor warps alternate
+// Sweep 2 lags sweep 1 by kLag = 2 extra batches (the factor warps' budget: the
+// pow and, for G > 1, the L2 exchange round trip). Factor warps alternate
 // batches: 3 for G == 1, 2 when G > 1 (measured: more warps polling L2 cost
 // more issue slots than they buy).
-// TMEM-lag variant (sweep_tmem.cuh, UOT_TMEM=1): measured 2-3% slower than the
-// smem-ring kernel on B200 (profiles/r01_ncu_v3.md), kept as an opt-in.
-#ifndef UOT_LA_G1
-#define UOT_LA_G1 2
-#endif
-#ifndef UOT_LA_X
-#define UOT_LA_X 2
-#endif
-#ifndef UOT_NF_X
-#define UOT_NF_X 2
-#endif
-// TMEM-lag kernel: lag (batches in TMEM) and the load / store ring split.
-#ifndef UOT_TM_LA_X
-#define UOT_TM_LA_X 4
-#endif
-#ifndef UOT_TM_LA_G1
-#define UOT_TM_LA_G1 3
-#endif
-#ifndef UOT_TM_NL
-#define UOT_TM_NL 4
-#endif
-#ifndef UOT_TM_NS
-#define UOT_TM_NS 3
-#endif
-#ifndef UOT_TM_S2FIRST
-#define UOT_TM_S2FIRST 1
-#endif
+constexpr int kLag = 2;
+constexpr int kFactorWarpsG1 = 3;
+constexpr int kFactorWarpsX = 2;
 // Column factors of sweep 1 parked in TMEM (sweep.cuh, TB) for slices of 3-4
 // float4 per thread: frees the registers that otherwise spill (measured +5-8%
 // at 32768^2 .. 16384^2; at V = 2 the factors fit registers and TMEM loses).
-#ifndef UOT_TMEM_BETA
-#define UOT_TMEM_BETA 1
-#endif
 template <int NT, int V, int BM, int NB, bool XCHG = false>
 SweepCfg make_cfg() {
-  constexpr int LA = XCHG ? UOT_LA_X : UOT_LA_G1;
-#ifndef UOT_NF_G1
-#define UOT_NF_G1 3
-#endif
-  constexpr int NF = XCHG ? UOT_NF_X : UOT_NF_G1;
+  constexpr int NF = XCHG ? kFactorWarpsX : kFactorWarpsG1;
   SweepCfg c{};
   c.nt = NT;
   c.v = V;
@@ -100,20 +63,12 @@ SweepCfg make_cfg() {
   c.nbuf = NB;
   c.nf = NF;
   c.xchg = XCHG;
-  constexpr bool TB = UOT_TMEM_BETA && V >= 3;
-  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false, float, TB>;
-  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false, float, TB>;
+  constexpr bool TB = V >= 3;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, kLag, XCHG, NF, false, false, float, TB>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, kLag, XCHG, NF, true, false, float, TB>;
   c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true>;
   c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
-  c.persist[0] = persist_kernel<NT, V, BM, NB, LA, XCHG, NF, false>;
-  c.persist[1] = persist_kernel<NT, V, BM, NB, LA, XCHG, NF, true>;
-  static_assert(UOT_TM_NL + UOT_TM_NS == NB, "TMEM kernel rings use the same shared memory");
-  constexpr int LAT = XCHG ? UOT_TM_LA_X : UOT_TM_LA_G1;
-  c.la_tm = LAT;
-  c.iter_tm[0] = sweep_tmem_kernel<NT, V, BM, UOT_TM_NL, UOT_TM_NS, LAT, XCHG, NF, false, UOT_TM_S2FIRST>;
-  c.iter_tm[1] = sweep_tmem_kernel<NT, V, BM, UOT_TM_NL, UOT_TM_NS, LAT, XCHG, NF, true, UOT_TM_S2FIRST>;
-  c.smem_bytes_tm = &TmemSweepSmem<NT / 32, BM, UOT_TM_NL, UOT_TM_NS>::bytes;
   return c;
 }
 
@@ -144,8 +99,7 @@ const std::vector<ResidentCfg>& rcfg_table() {
 // 4096-double slices); the ring/TMEM/persistent variants are fp32-only.
 template <int NT, int V, int BM, int NB, bool XCHG = false>
 SweepCfg make_cfg_f64() {
-  constexpr int LA = XCHG ? UOT_LA_X : UOT_LA_G1;
-  constexpr int NF = XCHG ? UOT_NF_X : UOT_NF_G1;
+  constexpr int NF = XCHG ? kFactorWarpsX : kFactorWarpsG1;
   SweepCfg c{};
   c.nt = NT;
   c.v = V;
@@ -153,8 +107,8 @@ SweepCfg make_cfg_f64() {
   c.nbuf = NB;
   c.nf = NF;
   c.xchg = XCHG;
-  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false, double>;
-  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false, double>;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, kLag, XCHG, NF, false, false, double>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, kLag, XCHG, NF, true, false, double>;
   c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true, double>;
   c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true, double>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
@@ -178,11 +132,6 @@ const std::vector<SweepCfg>& cfg_table() {
       make_cfg<512, 3, 1, 7, true>(), make_cfg<512, 4, 1, 7, true>(),
   };
   return t;
-}
-
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
 }
 
 // ------------------------------------------------------------------- NCCL --
@@ -271,14 +220,12 @@ struct uot_ctx {
   int smid_map = 0;
   int dyn = 1;  // batches handed out by a global counter (SweepArgs::dyn)
   ulonglong2* mail = nullptr;  // [groups][kMail] batch picks of the group leaders
-  size_t smem_tm = 0;    // dynamic smem of the TMEM-lag iteration kernel
   // resident mode: the whole uot_iterate call is one persistent launch
   const ResidentCfg* rcfg = nullptr;
   unsigned rgrid = 0;
   size_t rsmem = 0;
   int rfull = 0;
-  bool use_tmem = false;  // iterations run sweep_tmem_kernel (opt-in: UOT_TMEM=1)
-  bool use_persist = false;  // uot_iterate is one persistent streaming launch (persist.cuh, opt-in)
+  bool resident_on = true;  // uot_set_resident: use rcfg when the problem fits
   bool wide = false;  // rows wider than #SMs slices: only the two-pass schedule (ablation.cuh) runs
 
   // device buffers
@@ -335,12 +282,12 @@ namespace {
 
 // G > 1 and one sweep CTA on every SM: address CTAs by %smid so the G CTAs of a
 // row group run on neighbouring SMs. Enabled only when a probe launch with the
-// sweep's footprint shows %smid is a permutation of [0, grid) (UOT_SMID_MAP=0 off).
+// sweep's footprint shows %smid is a permutation of [0, grid).
 int probe_smid_map(uot_ctx* ctx) {
   ctx->smid_map = 0;
   int nsm = 0;
   if (ctx->cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device), "attr")) return UOT_CUDA_ERROR;
-  if (ctx->G < 2 || static_cast<int>(ctx->grid) != nsm || !env_int("UOT_SMID_MAP", 1)) return UOT_OK;
+  if (ctx->G < 2 || static_cast<int>(ctx->grid) != nsm) return UOT_OK;
   unsigned* d = nullptr;
   CK(cudaMalloc(&d, ctx->grid * sizeof(unsigned)));
   CK(cudaFuncSetAttribute(smid_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem)));
@@ -366,14 +313,14 @@ int plan_layout(uot_ctx* ctx) {
   const bool f64 = ctx->dtype == UOT_F64;
   const unsigned epc = 16 / ctx->esz;  // elements per 16-byte chunk
   const unsigned smax = kSliceMax * 4 / ctx->esz;  // 32 KiB of elements
-  const unsigned xmax = static_cast<unsigned>(env_int("UOT_SLICE_MAX_XCHG", kSliceMaxXchg)) * 4 / ctx->esz;
+  const unsigned xmax = kSliceMaxXchg * 4 / ctx->esz;
   unsigned G = cols <= smax ? 1u : static_cast<unsigned>((cols + xmax - 1) / xmax);
   if (G > static_cast<unsigned>(ctx->sms)) {
     // Rows wider than one slice per SM: the fused sweep cannot hold a row across
     // the grid, so a single-rank session runs the paper's two-pass schedule
     // (ablation.cuh: warp-per-row and column kernels, any width, the same
     // arithmetic at 16 B per element) for the seed and every iteration.
-    if (ctx->nranks > 1 || !env_int("UOT_WIDE", 1))
+    if (ctx->nranks > 1)
       return ctx->fail(UOT_CONFIG_ERROR, "cols %llu needs %u CTAs per row (max %d)",
                        (unsigned long long)cols, G, ctx->sms);
     ctx->wide = true;
@@ -403,19 +350,13 @@ int plan_layout(uot_ctx* ctx) {
   ctx->grid = ctx->groups * G;
   ctx->buf_stride = round_up(ctx->B * slice * ctx->esz, 128);
   ctx->smem = cfg->smem_bytes(ctx->buf_stride);
-  ctx->smem_tm = f64 ? 0 : cfg->smem_bytes_tm(ctx->buf_stride);
   int smem_optin = 0;
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  // the TMEM-lag kernel's rings + factor rings must fit next to each other
-  ctx->use_tmem = !f64 && env_int("UOT_TMEM", 0) != 0 && ctx->smem_tm <= static_cast<size_t>(smem_optin);
   ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * ctx->esz > (64ull << 20) ? 1 : 0;
-  // Dynamic batch schedule where per-SM bandwidth skew matters (streams past
-  // L2); smaller problems keep fixed row blocks: bit-reproducible run to run,
-  // like the reference's ordered reduction (UOT_DYNAMIC=0/1 forces either).
-  {
-    const int d = env_int("UOT_DYNAMIC", -1);
-    ctx->dyn = d < 0 ? ctx->evict_first : (d != 0);
-  }
+  // Row-batch schedule: fixed row blocks (bit-reproducible run to run, as the
+  // reference's ordered reduction) unless the caller opts into the dynamic
+  // batch counter with uot_set_deterministic(ctx, 0).
+  ctx->dyn = 0;
   ctx->full = slice == epc * cfg->nt * cfg->v ? 1 : 0;
   int rc = probe_smid_map(ctx);
   if (rc) return rc;
@@ -427,24 +368,10 @@ int plan_layout(uot_ctx* ctx) {
                              "cudaFuncSetAttribute(smem)");
     if (rc) return rc;
   }
-  if (ctx->use_tmem)
-    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(cfg->iter_tm[ctx->full]),
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_tm)));
-  // Persistent streaming mode (persist.cuh, opt-in UOT_PERSIST=1): single rank,
-  // the smem-ring kernel. Measured 2-6% slower per iteration than sweep +
-  // finalize (its loop body spills under the 96-register cap), so off by default.
-  // Every CTA must stream more than NBUF batches per iteration: the producer then
-  // never prefetches a row batch before its previous-iteration store was issued.
-  const uint64_t nb_min = (ctx->rows / ctx->groups) / ctx->B;
-  ctx->use_persist = !f64 && ctx->nranks == 1 && !ctx->use_tmem && env_int("UOT_PERSIST", 0) != 0 &&
-                     ctx->groups <= 160 && nb_min > static_cast<uint64_t>(cfg->nbuf);
-  if (ctx->use_persist)
-    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(cfg->persist[ctx->full]),
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem)));
   // Resident mode (resident.cuh): one rank, rows fit one CTA (G == 1), a CTA's
-  // row block fits shared memory and at most 32 rows per CTA. UOT_RESIDENT=0: off.
+  // row block fits shared memory and at most 32 rows per CTA (uot_set_resident).
   ctx->rcfg = nullptr;
-  if (!f64 && ctx->nranks == 1 && G == 1 && env_int("UOT_RESIDENT", 1)) {
+  if (!f64 && ctx->nranks == 1 && G == 1) {
     const unsigned rgrid = static_cast<unsigned>(std::min<uint64_t>(ctx->rows, ctx->sms));
     const uint64_t rows_cta = (ctx->rows + rgrid - 1) / rgrid;
     const unsigned nq = ctx->pitch / 4;
@@ -508,7 +435,6 @@ int create_common(uot_ctx* ctx, int device) {
     return ctx->fail(UOT_INVALID_PARAMETER, "device %d out of range (%d visible)", device, ndev);
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
-  ctx->sms = std::max(1, std::min(ctx->sms, env_int("UOT_SMS", ctx->sms)));  // experiments: cap the grid
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   int rc = plan_layout(ctx);
   if (rc) return rc;
@@ -570,13 +496,12 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
   // SM) makes that a permutation, even for the seed sweep, when other kernels
   // share the GPU (e.g. the ranks of a session group on one device)
   const bool xchg = ctx->G > 1;
-  const bool tm = !seed && ctx->use_tmem;
-  SweepFn fn = seed ? ctx->cfg->seed[ctx->full] : (tm ? ctx->cfg->iter_tm[ctx->full] : ctx->cfg->iter[ctx->full]);
+  SweepFn fn = seed ? ctx->cfg->seed[ctx->full] : ctx->cfg->iter[ctx->full];
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctx->grid);
   // compute warps + producer warp + factor warp(s)
   lc.blockDim = dim3(ctx->cfg->nt + 32 * (1 + (seed ? 1 : ctx->cfg->nf)));
-  lc.dynamicSmemBytes = tm ? ctx->smem_tm : ctx->smem;
+  lc.dynamicSmemBytes = ctx->smem;
   lc.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // CTAs of a group spin on each other
@@ -644,31 +569,6 @@ int launch_ablation_iteration(uot_ctx* ctx) {
   else
     launch_ablation_kernels<float>(ctx);
   return ctx->cuda(cudaGetLastError(), "ablation launch");
-}
-
-// The whole iterate(k) call as one persistent streaming launch (persist.cuh).
-int launch_persist(uot_ctx* ctx, uint64_t k) {
-  PersistArgs p;
-  p.s = sweep_args(ctx);
-  p.cpd = ctx->cpd;
-  p.beta2w = ctx->beta2;
-  p.col_sums = ctx->col_sums;
-  p.bar = ctx->bar_flags;
-  p.cols = static_cast<unsigned>(ctx->cols);
-  p.grid = ctx->grid;
-  p.k = static_cast<unsigned>(std::min<uint64_t>(k, 0xffffffffu));
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(ctx->grid);
-  lc.blockDim = dim3(ctx->cfg->nt + 32 * (1 + ctx->cfg->nf));
-  lc.dynamicSmemBytes = ctx->smem;
-  lc.stream = ctx->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers + exchange need every CTA resident
-  attr[0].val.cooperative = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  ctx->launches++;
-  return ctx->cuda(cudaLaunchKernelEx(&lc, ctx->cfg->persist[ctx->full], p), "persistent sweep launch");
 }
 
 // The whole iterate(k) call as one cooperative launch (resident.cuh).
@@ -779,7 +679,8 @@ int check_marginals(uot_ctx* ctx, const double* rpd, const double* cpd, double e
   return UOT_OK;
 }
 
-int after_matrix_upload(uot_ctx* ctx) {
+// Zero the padding columns [cols, pitch) of an uploaded plan.
+int pad_after_upload(uot_ctx* ctx) {
   const unsigned gblocks = static_cast<unsigned>(ctx->sms) * 8;
   if (ctx->pitch > ctx->cols) {
     if (ctx->dtype == UOT_F64)
@@ -790,6 +691,14 @@ int after_matrix_upload(uot_ctx* ctx) {
                                                              ctx->pitch);
     ctx->launches++;
   }
+  CK(cudaGetLastError());
+  return UOT_OK;
+}
+
+int after_matrix_upload(uot_ctx* ctx) {
+  int rc = pad_after_upload(ctx);
+  if (rc) return rc;
+  const unsigned gblocks = static_cast<unsigned>(ctx->sms) * 8;
   CK(cudaMemsetAsync(ctx->dflag, 0, sizeof(int), ctx->stream));
   if (ctx->dtype == UOT_F64)
     validate_matrix_kernel<<<gblocks, 256, 0, ctx->stream>>>(static_cast<const double*>(ctx->P), ctx->rows,
@@ -981,6 +890,12 @@ int uot_set_deterministic(uot_ctx* ctx, int on) {
   return UOT_OK;
 }
 
+int uot_set_resident(uot_ctx* ctx, int on) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  ctx->resident_on = on != 0;
+  return UOT_OK;
+}
+
 int uot_set_variant(uot_ctx* ctx, int variant) {
   if (!ctx) return UOT_INVALID_PARAMETER;
   if (variant != UOT_VARIANT_FUSED && variant != UOT_VARIANT_TWO_PASS && variant != UOT_VARIANT_BASELINE)
@@ -1045,10 +960,8 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->rows_per_step = ctx->B;
   o->threads = ctx->cfg->nt + 32 * (1 + ctx->cfg->nf);
   o->chunks = ctx->cfg->v;
-  o->smem_bytes = static_cast<uint32_t>(ctx->use_tmem ? ctx->smem_tm : ctx->smem);
-  o->tmem = ctx->use_tmem ? 1 : 0;
-  o->resident = ctx->rcfg ? 1 : 0;
-  o->persist = ctx->use_persist ? 1 : 0;
+  o->smem_bytes = static_cast<uint32_t>(ctx->smem);
+  o->resident = ctx->rcfg && ctx->resident_on ? 1 : 0;
   o->dtype = ctx->dtype;
   o->dynamic = ctx->dyn;
   o->nbuf = ctx->cfg->nbuf;
@@ -1158,6 +1071,25 @@ int uot_set_fi(uot_ctx* ctx, double fi) {
   return UOT_OK;
 }
 
+int uot_set_iterate_input(uot_ctx* ctx, const void* a, int dtype, const double* rpd, const double* cpd,
+                          double fi) {
+  if (!ctx || !a || !rpd || !cpd) return UOT_INVALID_PARAMETER;
+  int rc = dtype_check(ctx, dtype, "uot_set_iterate_input");
+  if (rc) return rc;
+  if (!std::isfinite(fi)) return ctx->fail(UOT_INVALID_PARAMETER, "fi must be finite");
+  CK(cudaSetDevice(ctx->device));
+  ctx->have_problem = false;
+  CK(cudaMemcpy2DAsync(ctx->P, ctx->pitch * ctx->esz, a, ctx->cols * ctx->esz, ctx->cols * ctx->esz, ctx->rows,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->rpd, rpd, ctx->rows * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->cpd, cpd, ctx->cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  if ((rc = reset_state(ctx))) return rc;
+  if ((rc = pad_after_upload(ctx))) return rc;
+  ctx->fi = fi;
+  ctx->have_problem = true;
+  return UOT_OK;
+}
+
 int uot_set_plan(uot_ctx* ctx, const float* a) {
   if (!ctx || !a) return UOT_INVALID_PARAMETER;
   int rc = dtype_check(ctx, UOT_F32, "uot_set_plan");
@@ -1202,6 +1134,10 @@ int uot_set_col_sums(uot_ctx* ctx, const double* col_sums) {
   if (!ctx->have_problem) return ctx->fail(UOT_INVALID_PARAMETER, "no problem set");
   CK(cudaSetDevice(ctx->device));
   CK(cudaMemcpyAsync(ctx->col_sums, col_sums, ctx->cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  // A new FusedState re-opens a session that stopped on convergence (a failed
+  // one stays stopped): without this the beta-only finalize below would skip.
+  resume_control_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctl);
+  ctx->launches++;
   // Recompute beta(iter+1) from the given state; its error slot starts at zero.
   CK(cudaMemsetAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Control, err_beta), 0,
                      2 * sizeof(double), ctx->stream));
@@ -1259,11 +1195,7 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
   ctx->launches++;
   CK(cudaGetLastError());
   int rc;
-  const bool resident = ctx->rcfg != nullptr && ctx->variant == UOT_VARIANT_FUSED;
-  // 32-bit global batch indices inside the persistent kernel: long calls are split
-  const uint64_t nb_max = (ctx->rows + ctx->groups - 1) / ctx->groups / ctx->B + 1;
-  const uint64_t kchunk = std::max<uint64_t>(
-      1, std::min<uint64_t>((1ull << 30) / nb_max, static_cast<uint64_t>(env_int("UOT_PERSIST_CHUNK", 1 << 30))));
+  const bool resident = ctx->rcfg != nullptr && ctx->resident_on && ctx->variant == UOT_VARIANT_FUSED;
   if (ctx->variant != UOT_VARIANT_FUSED) {
     for (uint64_t i = 0; i < k; ++i) {
       if (ctx->timing) record(ctx, 3 * i);
@@ -1271,14 +1203,9 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
       if (ctx->timing) record(ctx, 3 * i + 1);
       if (ctx->timing) record(ctx, 3 * i + 2);
     }
-  } else if (resident || ctx->use_persist) {  // k iterations, one launch: sweeps, reductions, stop test inside
+  } else if (resident) {  // k iterations, one launch: sweeps, reductions, stop test inside
     if (ctx->timing) record(ctx, 0);
-    if (resident) {
-      if ((rc = launch_resident(ctx, k))) return rc;
-    } else {
-      for (uint64_t done = 0; done < k; done += kchunk)
-        if ((rc = launch_persist(ctx, std::min(kchunk, k - done)))) return rc;
-    }
+    if ((rc = launch_resident(ctx, k))) return rc;
     if (ctx->timing) record(ctx, 1);
   } else {
     for (uint64_t i = 0; i < k; ++i) {
@@ -1300,19 +1227,19 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
   }
   if (ctx->timing) {
     ctx->sweep_ms = ctx->fin_ms = 0.0;
-    if (resident || ctx->use_persist) {  // one launch: reported as sweep time, no separate finalize
+    if (resident) {  // one launch: reported as sweep time, no separate finalize
       float a = 0.f;
       cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
       ctx->sweep_ms = a;
     }
-    for (uint64_t i = 0; i < ((resident || ctx->use_persist) ? 0 : k); ++i) {
+    for (uint64_t i = 0; i < (resident ? 0 : k); ++i) {
       float a = 0.f, b = 0.f;
       cudaEventElapsedTime(&a, ctx->ev[3 * i], ctx->ev[3 * i + 1]);
       cudaEventElapsedTime(&b, ctx->ev[3 * i + 1], ctx->ev[3 * i + 2]);
       ctx->sweep_ms += a;
       ctx->fin_ms += b;
     }
-    ctx->sweeps_timed = (resident || ctx->use_persist) ? std::max<uint64_t>(1, ctx->h_ctl->iter - before) : k;
+    ctx->sweeps_timed = resident ? std::max<uint64_t>(1, ctx->h_ctl->iter - before) : k;
   }
   if (iterations) *iterations = ctx->h_ctl->iter - before;
   if (final_error) *final_error = ctx->h_ctl->last_error;

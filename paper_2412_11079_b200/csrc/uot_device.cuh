@@ -54,11 +54,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 __device__ __forceinline__ bool rescale_factor_dev(double target, double sum, double fi,
                                                    double* out) {
   if (!(sum > 0.0)) return false;
-#ifdef UOT_FAST_POW
-  const double f = exp2(fi * log2(target / sum));
-#else
   const double f = pow(target / sum, fi);
-#endif
   if (!(f > 0.0) || !isfinite(f)) return false;
   *out = f;
   return true;

@@ -88,8 +88,8 @@ class Layout(C.Structure):
                 ("threads", C.c_uint32), ("chunks", C.c_uint32), ("smem_bytes", C.c_uint32),
                 ("nbuf", C.c_uint32), ("sms", C.c_uint32), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("device", C.c_int32), ("evict_first", C.c_int32),
-                ("smid_map", C.c_int32), ("exchange", C.c_int32), ("tmem", C.c_int32),
-                ("resident", C.c_int32), ("persist", C.c_int32), ("dtype", C.c_int32),
+                ("smid_map", C.c_int32), ("exchange", C.c_int32),
+                ("resident", C.c_int32), ("dtype", C.c_int32),
                 ("dynamic", C.c_int32), ("variant", C.c_int32)]
 
     def as_dict(self):
@@ -128,6 +128,7 @@ def lib():
     L.uot_group_iterate.argtypes = [_P, _i, _u64, _d, C.POINTER(_u64), C.POINTER(_d), C.POINTER(_i)]
     L.uot_set_variant.argtypes = [_P, _i]
     L.uot_set_deterministic.argtypes = [_P, _i]
+    L.uot_set_resident.argtypes = [_P, _i]
     L.uot_problem_file_info.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_i),
                                         C.POINTER(_d), C.POINTER(_d)]
     L.uot_last_io_error.restype = C.c_char_p
@@ -147,6 +148,7 @@ def lib():
     L.uot_gen_block_f64.argtypes = [_u64, _u64, _u64, _u64, _u64, _P, _P, _P, _i]
     L.uot_generate_problem.argtypes = [_P, _u64, _d, _d]
     L.uot_set_plan.argtypes = [_P, _P]
+    L.uot_set_iterate_input.argtypes = [_P, _P, _i, _P, _P, _d]
     L.uot_set_fi.argtypes = [_P, _d]
     L.uot_init_col_sums.argtypes = [_P]
     L.uot_set_col_sums.argtypes = [_P, _P]
@@ -486,6 +488,19 @@ class Session:
         session's marginals and er/ep (collective over the ranks)."""
         self._check(lib().uot_save_problem_file(self._h, os.fsencode(path)))
 
+    def set_iterate_input(self, a: np.ndarray, rpd: np.ndarray, cpd: np.ndarray, fi: float):
+        """fused_iterate's inputs as given (uot_set_iterate_input): the current
+        plan, marginals and fi, without require_valid's checks."""
+        a = np.ascontiguousarray(a, self.dtype)
+        if a.shape != (self.rows, self.cols):
+            _raise(1, f"matrix shape {a.shape} does not match the session ({self.rows}, {self.cols})")
+        rpd = np.ascontiguousarray(rpd, np.float64)
+        cpd = np.ascontiguousarray(cpd, np.float64)
+        if rpd.size != self.rows or cpd.size != self.cols:
+            _raise(1, "marginal lengths do not match the matrix")
+        code = UOT_F64 if self.dtype == np.float64 else UOT_F32
+        self._check(lib().uot_set_iterate_input(self._h, _ptr(a), code, _ptr(rpd), _ptr(cpd), float(fi)))
+
     def set_fi(self, fi: float):
         self._check(lib().uot_set_fi(self._h, float(fi)))
 
@@ -565,10 +580,18 @@ class Session:
         self._check(lib().uot_set_variant(self._h, self.VARIANTS[name]))
 
     def set_deterministic(self, on: bool = True):
-        """Fixed row blocks per CTA group (bit-reproducible run to run) instead
-        of the default dynamic batch schedule (uot_set_deterministic)."""
+        """Fixed row blocks per CTA group (the default: bit-reproducible run to
+        run), or with on=False the dynamic batch counter (uot_set_deterministic)."""
         self._check(lib().uot_set_deterministic(self._h, 1 if on else 0))
         self.layout["dynamic"] = 0 if on else 1
+
+    def set_resident(self, on: bool = True):
+        """Allow (default) or forbid the one-launch resident solve for small
+        problems (uot_set_resident)."""
+        self._check(lib().uot_set_resident(self._h, 1 if on else 0))
+        lay = Layout()
+        lib().uot_get_layout(self._h, C.byref(lay))
+        self.layout = lay.as_dict()
 
     def set_timing(self, on: bool = True):
         self._check(lib().uot_set_timing(self._h, 1 if on else 0))
@@ -717,19 +740,24 @@ def init_col_sums(a: np.ndarray, device: int = 0) -> np.ndarray:
 def fused_iterate(a: np.ndarray, state: FusedState, p: Problem, fi: float, device: int = 0,
                   session: Session | None = None) -> ScalingFactors:
     """fused_iterate (fused.hpp:164-191) with the reference's host-in/host-out
-    contract: `a` and `state.col_sums` are updated in place. Each call moves the
-    matrix over PCIe; keep a Session for device-resident loops."""
+    contract: `a` and `state.col_sums` are updated in place. Matrix<float> or
+    Matrix<double> by a's dtype (Problem<double> iterates in f64, as the
+    reference's template does). Like the reference it checks only shapes: the
+    current plan and fi are used as given (no require_valid). Each call moves
+    the matrix over PCIe; keep a Session for device-resident loops."""
     if a.shape != (p.m(), p.n()):
         _raise(1, "fused_iterate: matrix shape does not match problem")
     if np.asarray(state.col_sums).size != p.n():
         _raise(1, "fused_iterate: carried column sums have wrong length")
-    s = session if session is not None else _cached_session(p.m(), p.n(), device)
-    s.set_problem(Problem(a, p.rpd, p.cpd, p.er, p.ep))
-    s.set_fi(fi)  # the caller's exponent, bit for bit
+    dt = np.dtype(np.float64 if a.dtype == np.float64 else np.float32)
+    s = session if session is not None else _cached_session(p.m(), p.n(), device, dt)
+    if s.dtype != dt:
+        _raise(1, f"fused_iterate: a {a.dtype} matrix on a {s.dtype} session")
+    s.set_iterate_input(a, p.rpd, p.cpd, fi)
     s.set_col_sums(state.col_sums)
     s.iterate(1, 1e-300)
     f = s.factors()
-    s.plan(out=a) if a.flags.c_contiguous and a.dtype == np.float32 else a.__setitem__(Ellipsis, s.plan())
+    s.plan(out=a) if a.flags.c_contiguous and a.dtype == dt else a.__setitem__(Ellipsis, s.plan())
     state.col_sums = s.col_sums()
     return f
 
@@ -737,13 +765,14 @@ def fused_iterate(a: np.ndarray, state: FusedState, p: Problem, fi: float, devic
 _tls = threading.local()
 
 
-def _cached_session(m: int, n: int, device: int) -> "Session":
-    """One fp32 session per thread and (shape, device), kept between fused_iterate
-    calls: a loop pays the two PCIe transfers per call, not a session setup."""
-    key = (int(m), int(n), int(device))
+def _cached_session(m: int, n: int, device: int, dtype=np.float32) -> "Session":
+    """One session per thread and (shape, device, dtype), kept between
+    fused_iterate calls: a loop pays the two PCIe transfers per call, not a
+    session setup."""
+    key = (int(m), int(n), int(device), np.dtype(dtype).str)
     s = getattr(_tls, "session", None)
     if s is None or getattr(_tls, "key", None) != key or not s._h:
         if s is not None:
             s.close()
-        _tls.session, _tls.key = Session(m, n, device), key
+        _tls.session, _tls.key = Session(m, n, device, dtype=dtype), key
     return _tls.session

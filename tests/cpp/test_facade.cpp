@@ -258,6 +258,55 @@ void test_worker_plan_overloads() {  // fused.hpp:197-208, 259-285: same call sh
   CHECK_THROWS_AS(uot::cuda::fused_iterate_parallel(ga, gs, p, fi, plan, small), uot::InvalidParameter);
 }
 
+void test_integral_fourth_argument_means_workers() {  // fused.hpp:287-291 call shapes
+  // uot::fused_solve(p, tol, it, 8) is 8 workers; switched by namespace it must
+  // stay 8 workers on device 0 (a one-GPU box has no device 8), for every
+  // integral type a call site may pass.
+  const auto p = random_problem(28, 96, 130, 0.5);
+  const auto ref = uot::fused_solve(p, kNever, 10, 8);
+  const auto a = uot::cuda::fused_solve(p, kNever, 10, 8);
+  const auto b = uot::cuda::fused_solve(p, kNever, 10, 8u);
+  const auto c = uot::cuda::fused_solve(p, kNever, 10, 8L);
+  const auto d = uot::cuda::fused_solve(p, kNever, 10, std::size_t(8));
+  const auto e = uot::cuda::fused_solve(p, kNever, 10, uot::cuda::Device{0});
+  const auto f = uot::cuda::fused_solve(p, kNever, 10, 3, uot::cuda::Device{0});
+  for (const auto* r : {&a, &b, &c, &d, &e, &f}) {
+    CHECK(r->report.iterations == 10);
+    CHECK(max_rel(r->plan, ref.plan) <= 1e-5);
+  }
+  CHECK(a.plan == b.plan && a.plan == d.plan && a.plan == e.plan);
+  CHECK_THROWS_AS(uot::cuda::fused_solve(p, kNever, 10, 0), uot::InvalidParameter);
+  CHECK_THROWS_AS(uot::cuda::fused_solve(p, kNever, 10, -2), uot::InvalidParameter);
+}
+
+void test_fused_iterate_takes_inputs_as_given() {  // fused.hpp:164-191: shape checks only
+  // a zero plan entry and an unvalidated Problem (ep < 0 would fail
+  // require_valid) iterate exactly like the reference's fused_iterate
+  auto p = random_problem(29, 40, 64, 0.5);
+  p.ep = -0.5;
+  uot::Matrix<float> mine = p.a, theirs = p.a;
+  mine(3, 5) = theirs(3, 5) = 0.f;
+  uot::FusedState sm{uot::init_col_sums(mine)}, st{uot::init_col_sums(theirs)};
+  for (int it = 0; it < 4; ++it) {
+    const auto fm = uot::cuda::fused_iterate(mine, sm, p, 0.7);
+    const auto ft = uot::fused_iterate(theirs, st, p, 0.7);
+    CHECK(uot::max_abs_diff(fm.alpha, ft.alpha) <= 1e-13);
+    CHECK(uot::max_abs_diff(fm.beta, ft.beta) <= 1e-13);
+  }
+  CHECK(mine == theirs);
+  // Matrix<double>: the f64 kernel, as the reference template with T = double
+  auto pd = uot::gen_problem_t<double>(30, 33, 50);
+  uot::Matrix<double> md = pd.a, td = pd.a;
+  uot::FusedState sd{uot::init_col_sums(md)}, tsd{uot::init_col_sums(td)};
+  for (int it = 0; it < 3; ++it) {
+    uot::cuda::fused_iterate(md, sd, pd, 0.6);
+    uot::fused_iterate(td, tsd, pd, 0.6);
+  }
+  double m = 0.0;
+  for (std::size_t k = 0; k < md.size(); ++k) m = std::max(m, std::abs(md.data()[k] - td.data()[k]) / td.data()[k]);
+  CHECK(m <= 1e-13);
+}
+
 }  // namespace
 
 int main() {
@@ -274,6 +323,8 @@ int main() {
       {"Problem<double>", test_f64_problem_matches_reference},
       {"in-process ranks (reference signature)", test_in_process_ranks_match_reference},
       {"WorkerPlan overloads", test_worker_plan_overloads},
+      {"integral 4th argument = workers", test_integral_fourth_argument_means_workers},
+      {"fused_iterate inputs as given", test_fused_iterate_takes_inputs_as_given},
   };
   for (const auto& [name, fn] : cases) {
     const int before = g_fail;

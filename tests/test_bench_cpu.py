@@ -11,7 +11,7 @@ from conftest import ROOT
 
 def test_reference_arm_prints_one_contract_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2",
-                          "--warmup", "3", "--cpu-sample-rows", "64"], capture_output=True, text=True, timeout=600,
+                          "--warmup", "3", "--rows", "64"], capture_output=True, text=True, timeout=600,
                          cwd=ROOT)
     assert out.returncode == 0, out.stderr
     lines = [l for l in out.stdout.splitlines() if l.strip()]
@@ -21,3 +21,33 @@ def test_reference_arm_prints_one_contract_line():
     assert d["value"] > 0 and d["higher_is_better"] is True
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["w1"]["workers"] == 1 and d["config"]["same_config"] is True
+
+
+def test_reference_arm_n2_runs_on_rank0_only():
+    """Under torchrun the reference arm's rank 0 prints the line, other ranks exit 0."""
+    env = dict(os.environ, WORLD_SIZE="2", RANK="1", LOCAL_RANK="1")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "3", "--rows", "32"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0 and out.stdout.strip() == "", out.stderr
+    env["RANK"] = env["LOCAL_RANK"] = "0"
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "3", "--rows", "32"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+def test_plain_multi_gpu_invocation_spawns_ranks():
+    """`python bench.py --gpus 2` (no torchrun) re-launches itself with one process
+    per GPU; here (no GPU) both ranks get past argument parsing and the gloo
+    rendezvous and fail at device-session creation, not in the launcher."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--no-e2e", "--steps", "3",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode != 0  # no CUDA device in this container
+    err = out.stderr
+    assert "usage:" not in err and "error: argument" not in err
+    assert err.count("CudaError") >= 2 or err.count("CUDA") >= 2, err[-3000:]

@@ -3,19 +3,16 @@
 * streaming: one sweep launch + one finalize launch per iteration (sweep.cuh,
   finalize.cuh) — any shape;
 * resident: the whole call is ONE cooperative launch with the matrix in shared
-  memory and two grid barriers per iteration (resident.cuh) — small shapes;
-* TMEM lag (opt-in): the streaming sweep with the alpha lag parked in Tensor
-  Memory (sweep_tmem.cuh);
-* persistent streaming (opt-in): all k iterations in one launch of the ring
-  kernel, the finalize replaced by grid barriers (persist.cuh).
+  memory and two grid barriers per iteration (resident.cuh) — small shapes
+  (uot_set_resident(ctx, 0) forces streaming);
+* the two row-batch schedules of the streaming sweep: fixed row blocks (the
+  default, bit-reproducible) and the dynamic batch counter.
 
 Each mode is checked against the CPU oracle (fused_solve, fused.hpp:259-291)
 and the modes against each other, including the early exit and the
 degenerate-sum paths the reference defines (fused.hpp:273-281, scaling.cpp:15-22).
 """
 from __future__ import annotations
-
-import os
 
 import numpy as np
 import pytest
@@ -26,27 +23,20 @@ from test_gpu_parity import assert_parity
 pytestmark = pytest.mark.gpu
 
 
-def run(uot, a, rpd, cpd, er, ep, k, tol=KNEVER, env=None, chunks=None):
-    old = {key: os.environ.get(key) for key in (env or {})}
-    os.environ.update(env or {})
-    try:
-        with uot.Session(a.shape[0], a.shape[1]) as s:
-            lay = s.layout
-            s.set_problem(uot.Problem(a, rpd, cpd, er, ep))
-            s.init_col_sums()
-            done = 0
-            for c in (chunks or [k]):
-                it, err, conv = s.iterate(c, tol)
-                done += it
-                if conv:
-                    break
-            return s.plan(), s.factors(), s.col_sums(), done, err, conv, lay
-    finally:
-        for key, v in old.items():
-            if v is None:
-                os.environ.pop(key, None)
-            else:
-                os.environ[key] = v
+def run(uot, a, rpd, cpd, er, ep, k, tol=KNEVER, resident=True, chunks=None, deterministic=True):
+    with uot.Session(a.shape[0], a.shape[1]) as s:
+        s.set_resident(resident)
+        s.set_deterministic(deterministic)
+        lay = s.layout
+        s.set_problem(uot.Problem(a, rpd, cpd, er, ep))
+        s.init_col_sums()
+        done = 0
+        for c in (chunks or [k]):
+            it, err, conv = s.iterate(c, tol)
+            done += it
+            if conv:
+                break
+        return s.plan(), s.factors(), s.col_sums(), done, err, conv, lay
 
 
 @pytest.mark.parametrize("m,n,k", [(1024, 1024, 40), (2000, 513, 30), (16, 16, 25), (3, 7, 9), (300, 4096, 12)])
@@ -54,7 +44,7 @@ def test_resident_matches_streaming_and_oracle(gpu, orc, m, n, k):
     a, rpd, cpd = orc.gen_problem(42, m, n)
     ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 4)
     res = run(gpu, a, rpd, cpd, 1.0, 0.1, k)
-    stream = run(gpu, a, rpd, cpd, 1.0, 0.1, k, env={"UOT_RESIDENT": "0"})
+    stream = run(gpu, a, rpd, cpd, 1.0, 0.1, k, resident=False)
     assert res[6]["resident"] == 1 and stream[6]["resident"] == 0
     for plan, f, cs, it, err, conv, lay in (res, stream):
         assert it == k
@@ -96,47 +86,11 @@ def test_resident_degenerate_column_sums_raise(gpu, orc):
         np.testing.assert_array_equal(s.plan(), a)
 
 
-@pytest.mark.parametrize("m,n,k", [(4096, 4096, 8), (64, 32768, 6), (700, 20000, 5)])
-def test_tmem_lag_variant_matches_oracle(gpu, orc, m, n, k):
-    a, rpd, cpd = orc.gen_problem(42, m, n)
-    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 8)
-    plan, f, cs, it, err, conv, lay = run(gpu, a, rpd, cpd, 1.0, 0.1, k, env={"UOT_TMEM": "1"})
-    assert lay["tmem"] == 1 and it == k
-    assert_parity(plan, ref.plan, rpd, cpd, f"tmem {m}x{n}")
-    np.testing.assert_allclose(f.alpha, ref.alpha, rtol=1e-12)
-
-
-@pytest.mark.parametrize("m,n,k", [(4096, 4096, 9), (1500, 20000, 6), (3000, 4096, 12)])
-def test_persistent_streaming_matches_oracle(gpu, orc, m, n, k):
-    a, rpd, cpd = orc.gen_problem(42, m, n)
-    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 8)
-    env = {"UOT_PERSIST": "1", "UOT_RESIDENT": "0"}
-    plan, f, cs, it, err, conv, lay = run(gpu, a, rpd, cpd, 1.0, 0.1, k, env=env)
-    assert lay["persist"] == 1 and it == k
-    assert_parity(plan, ref.plan, rpd, cpd, f"persist {m}x{n}")
-    # f64 sums in another order can flip the last bit of a stored f32 entry,
-    # which moves that column's sum by ~ulp(x)/rows
-    np.testing.assert_allclose(f.alpha, ref.alpha, rtol=1e-10)
-    np.testing.assert_allclose(cs, ref.col_sums, rtol=1e-8)
-    assert abs(err - ref.final_error) <= 1e-9 * max(1.0, ref.final_error)
-    split = run(gpu, a, rpd, cpd, 1.0, 0.1, k, env=env, chunks=[2, k - 2])
-    assert np.array_equal(split[0], plan)
-
-
-def test_persistent_streaming_early_exit(gpu, orc):
-    a, rpd, cpd = orc.gen_problem(5, 6000, 2048)
-    cpd = cpd * (rpd.sum() / cpd.sum())
-    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.0, 1e-6, 10000, 1)
-    r = run(gpu, a, rpd, cpd, 1.0, 0.0, 10000, tol=1e-6, env={"UOT_PERSIST": "1", "UOT_RESIDENT": "0"})
-    assert r[6]["persist"] == 1 and ref.converged and r[5] and r[3] == ref.iterations
-    assert_parity(r[0], ref.plan, rpd, cpd, "persist converged")
-
-
 @pytest.mark.parametrize("m,n,k", [(3000, 32768, 4), (20000, 4096, 5), (4099, 8192, 4)])
 def test_batch_schedules(gpu, orc, m, n, k):
-    """Dynamic batches (default: a device counter hands out row batches) and the
-    deterministic schedule (fixed row blocks, uot_set_deterministic) both meet the
-    parity bar; the deterministic one reproduces itself bit for bit."""
+    """The deterministic schedule (default: fixed row blocks) and dynamic batches
+    (a device counter hands out row batches, uot_set_deterministic(0)) both meet
+    the parity bar; the deterministic one reproduces itself bit for bit."""
     a, rpd, cpd = orc.gen_problem(11, m, n)
     ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 4)
     out = {}

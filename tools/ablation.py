@@ -17,9 +17,8 @@ shapes = [tuple(int(v) for v in s.split("x")) for s in args] or [(32768, 32768, 
 rows = []
 for m, n, k in shapes:
     for var in ("fused", "two_pass", "baseline"):
-        import os
-        os.environ["UOT_RESIDENT"] = "0"
         with uot.Session(m, n) as s:
+            s.set_resident(False)
             s.generate_problem(42, 1.0, 0.1)
             s.init_col_sums()
             s.set_variant(var)

@@ -43,10 +43,8 @@ for (m, n, k) in shapes:
           f"nt={lay['threads']} v={lay['chunks']} B={lay['rows_per_step']} ({dt:.2f}s) {'OK' if good else 'FAIL'}",
           flush=True)
 
-import os
-for (m, n, k, lag) in [(32768, 32768, 20, "8192"), (262144, 4096, 20, "8192"),
-                       (8192, 8192, 100, "8192"), (1024, 1024, 200, "8192"), (131072, 32768, 5, "8192")]:
-    os.environ["UOT_SLICE_MAX_XCHG"] = lag
+for (m, n, k) in [(32768, 32768, 20), (262144, 4096, 20), (8192, 8192, 100), (1024, 1024, 200),
+                  (131072, 32768, 5)]:
     with uot.Session(m, n) as s:
         s.generate_problem(42, ER, EP)
         s.init_col_sums()
@@ -57,6 +55,6 @@ for (m, n, k, lag) in [(32768, 32768, 20, "8192"), (262144, 4096, 20, "8192"),
         wall = time.time() - t0
         sw, fin, n_ = s.timing()
         gbs = 2 * m * n * 4 / (sw / n_ * 1e-3) / 1e9
-        print(f"{m}x{n} xslice={lag}: sweep {sw / n_:.3f} ms/iter ({gbs:.0f} GB/s), finalize {fin / n_ * 1e3:.1f} us/iter, "
+        print(f"{m}x{n}: sweep {sw / n_:.3f} ms/iter ({gbs:.0f} GB/s), finalize {fin / n_ * 1e3:.1f} us/iter, "
               f"wall {wall / k * 1e3:.3f} ms/iter, layout {s.layout}", flush=True)
 print("ALL OK" if ok else "SOME FAILED")

@@ -16,6 +16,7 @@ esz = 8 if f64 else 4
 for spec in [a for a in sys.argv[1:] if not a.startswith("--")]:
     m, n, k = (int(x) for x in spec.split("x"))
     with uot.Session(m, n, dtype=np.float64 if f64 else np.float32) as s:
+        s.set_deterministic("--dynamic" not in sys.argv)
         s.generate_problem(42, 1.0, 0.1)
         s.init_col_sums()
         s.set_timing(True)
@@ -25,5 +26,5 @@ for spec in [a for a in sys.argv[1:] if not a.startswith("--")]:
         gbs = 2 * m * n * esz / (sw / n_ * 1e-3) / 1e9
         lay = s.layout
         print(f"[{tag}{' f64' if f64 else ''}] {m}x{n}: sweep {sw / n_ * 1e3:.1f} us ({gbs:.0f} GB/s) finalize {fin / n_ * 1e3:.1f} us "
-              f"G={lay["G"]} per={lay["persist"]} res={lay["resident"]} tm={lay["tmem"]} smid={lay["smid_map"]} groups={lay["groups"]} B={lay['rows_per_step']} thr={lay['threads']} v={lay['chunks']}",
+              f"G={lay["G"]} res={lay["resident"]} dyn={lay["dynamic"]} smid={lay["smid_map"]} groups={lay["groups"]} B={lay['rows_per_step']} thr={lay['threads']} v={lay['chunks']}",
               flush=True)
