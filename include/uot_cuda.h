@@ -87,7 +87,9 @@ UOT_API int uot_create(uot_ctx** out, uint64_t rows, uint64_t cols, int dtype, i
  * RankPartition::make(nranks, global_rows).blocks[rank] (src/plan.cpp:35-44;
  * PartitionError when nranks > global_rows) and joins the NCCL communicator
  * identified by `nccl_id` (128 bytes from uot_nccl_unique_id on rank 0).
- * Replaces distributed_solve's rank state (distributed.hpp:65-79). */
+ * Replaces distributed_solve's rank state (distributed.hpp:65-79). nranks == 1
+ * with a non-NULL id builds a one-rank communicator and runs the same NCCL
+ * exchange path (NULL: a plain single-GPU session). */
 UOT_API int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtype, int device,
                     int rank, int nranks, const uint8_t* nccl_id);
 UOT_API int uot_nccl_unique_id(uint8_t* out128);

@@ -643,7 +643,7 @@ int launch_finalize_dist(uot_ctx* ctx) {
 
 template <int MODE>
 int launch_finalize(uot_ctx* ctx) {
-  return ctx->nranks > 1 ? launch_finalize_dist<MODE>(ctx) : launch_finalize_single<MODE>(ctx);
+  return ctx->xmode != kXchNone ? launch_finalize_dist<MODE>(ctx) : launch_finalize_single<MODE>(ctx);
 }
 
 int sync_ctl(uot_ctx* ctx) {
@@ -808,7 +808,9 @@ int uot_create_dist(uot_ctx** out, uint64_t global_rows, uint64_t cols, int dtyp
   int rc = create_rank(out, global_rows, cols, dtype, device, rank, nranks);
   if (rc) return rc;
   uot_ctx* ctx = *out;
-  if (nranks > 1) {
+  // nranks == 1 with an id: a one-rank communicator, so the NCCL exchange path
+  // (reduce -> ncclAllReduce -> beta) runs and can be tested on one GPU.
+  if (nranks > 1 || nccl_id) {
     ctx->xmode = kXchNccl;
     if (!nccl_id) return ctx->fail(UOT_INVALID_PARAMETER, "a multi-rank session needs the NCCL id of rank 0");
     if (!nccl().ok) return ctx->fail(UOT_NCCL_ERROR, "%s", nccl().err.c_str());
@@ -961,7 +963,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->threads = ctx->cfg->nt + 32 * (1 + ctx->cfg->nf);
   o->chunks = ctx->cfg->v;
   o->smem_bytes = static_cast<uint32_t>(ctx->smem);
-  o->resident = ctx->rcfg && ctx->resident_on ? 1 : 0;
+  o->resident = ctx->rcfg && ctx->resident_on && ctx->xmode == kXchNone ? 1 : 0;
   o->dtype = ctx->dtype;
   o->dynamic = ctx->dyn;
   o->nbuf = ctx->cfg->nbuf;
@@ -1195,7 +1197,8 @@ int uot_iterate_timed(uot_ctx* ctx, uint64_t k, double tol, uint64_t* iterations
   ctx->launches++;
   CK(cudaGetLastError());
   int rc;
-  const bool resident = ctx->rcfg != nullptr && ctx->resident_on && ctx->variant == UOT_VARIANT_FUSED;
+  const bool resident =
+      ctx->rcfg != nullptr && ctx->resident_on && ctx->xmode == kXchNone && ctx->variant == UOT_VARIANT_FUSED;
   if (ctx->variant != UOT_VARIANT_FUSED) {
     for (uint64_t i = 0; i < k; ++i) {
       if (ctx->timing) record(ctx, 3 * i);

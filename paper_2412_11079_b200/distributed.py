@@ -83,7 +83,7 @@ class DistSession(uot.Session):
             raise uot.InvalidParameter(f"exchange must be 'peer' or 'nccl', not {exchange!r}")
         if exchange == "nccl" and nranks > 1 and nccl_id is None:
             raise uot.InvalidParameter("a multi-rank NCCL session needs the NCCL id of rank 0")
-        dist = (rank, nranks, "peer") if exchange == "peer" else (rank, nranks, nccl_id or b"\0" * 128)
+        dist = (rank, nranks, "peer") if exchange == "peer" else (rank, nranks, nccl_id)
         super().__init__(global_rows, cols, device, dist=dist)
         self.rank, self.nranks, self.exchange = rank, nranks, exchange
 

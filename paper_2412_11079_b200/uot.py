@@ -409,9 +409,12 @@ class Session:
                                    int(rank), int(nranks))
         else:
             rank, nranks, nccl_id = dist
-            idbuf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id).ljust(128, b"\0"))
+            idp = None  # NULL: a one-rank session without a communicator
+            if nccl_id is not None:
+                idbuf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id).ljust(128, b"\0"))
+                idp = C.cast(idbuf, _P)
             rc = L.uot_create_dist(C.byref(self._h), int(rows), int(cols), code, int(device),
-                                   int(rank), int(nranks), C.cast(idbuf, _P))
+                                   int(rank), int(nranks), idp)
         if rc:
             msg = self._err()
             self.close()

@@ -54,7 +54,8 @@ def solve(rank, world, out, seed, rows, cols, k, tol, ep, balance=0):
     from paper_2412_11079_b200 import distributed as D
     from paper_2412_11079_b200 import uot
     exchange = os.environ.get("UOT_EXCHANGE", "peer")
-    device = int(os.environ.get("MR_DEVICE", "0"))
+    md = os.environ.get("MR_DEVICE", "0")
+    device = rank if md == "rank" else int(md)  # "rank": one GPU per rank
     b, e = uot.RankPartition.make(world, rows).blocks[rank]
     p = uot.gen_block(seed, rows, cols, b, e - b)
     p.er, p.ep = 1.0, ep

@@ -123,3 +123,83 @@ def test_three_ranks_one_gpu_peer_exchange(gpu, orc, tmp_path):
     run_ranks(3, "solve", str(tmp_path), 3, 257, 1000, 8, KNEVER, 0.1,
               env_extra={"UOT_EXCHANGE": "peer", "MR_DEVICE": "0"})
     _check_solve(tmp_path, orc, 3, 257, 1000, 8, KNEVER, 0.1, seed=3)
+
+
+# ------------------------------------------------ NCCL / cross-device paths --
+
+def _ngpus() -> int:
+    try:
+        import torch
+        return torch.cuda.device_count() if torch.cuda.is_available() else 0
+    except ImportError:
+        return 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols,k", [(300, 2000, 10), (64, 20000, 6)])
+def test_single_rank_nccl_exchange_path(gpu, orc, rows, cols, k):
+    """uot_create_dist with one rank and an NCCL id runs the NCCL exchange path
+    (stage-1 reduce -> ncclAllReduce over a one-rank communicator -> stage-2
+    beta, allreduce.cpp:6-15 with P = 1) on one GPU; == distributed_solve(1)."""
+    from paper_2412_11079_b200 import distributed as D
+    a, rpd, cpd = orc.gen_problem(42, rows, cols)
+    ref = orc.distributed_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 1)
+    s = D.DistSession(rows, cols, 0, 1, 0, D.nccl_unique_id(), "nccl")
+    try:
+        assert s.exchange_mode() == 1 and s.layout["resident"] == 0
+        s.set_problem(gpu.Problem(a, rpd, cpd, 1.0, 0.1))
+        s.init_col_sums()
+        it, err, conv = s.iterate(k, KNEVER)
+        f = s.factors()
+        plan = s.plan()
+        calls, dbl = s.comm_stats()
+    finally:
+        s.close()
+    assert it == k and calls == k and dbl == k * cols
+    rel = np.max(np.abs(plan.astype(np.float64) - ref.plan) / ref.plan)
+    assert rel <= 1e-5
+    np.testing.assert_allclose(f.beta, ref.beta, rtol=1e-12)
+    np.testing.assert_allclose(f.alpha, ref.alpha, rtol=1e-12)
+    assert abs(err - ref.final_error) <= 1e-9 * max(1.0, ref.final_error)
+
+
+@pytest.mark.gpu
+def test_single_rank_nccl_early_exit(gpu, orc):
+    from paper_2412_11079_b200 import distributed as D
+    a, rpd, cpd = orc.gen_problem(5, 200, 3000)
+    cpd = cpd * (rpd.sum() / cpd.sum())
+    ref = orc.distributed_solve(a, rpd, cpd, 1.0, 0.0, 1e-6, 10000, 1)
+    s = D.DistSession(200, 3000, 0, 1, 0, D.nccl_unique_id(), "nccl")
+    try:
+        s.set_problem(gpu.Problem(a, rpd, cpd, 1.0, 0.0))
+        s.init_col_sums()
+        it, err, conv = s.iterate(10000, 1e-6)
+    finally:
+        s.close()
+    assert ref.converged and conv and it == ref.iterations
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs (gpurun and the round-end box have one)")
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+def test_two_ranks_two_gpus(gpu, orc, tmp_path, exchange):
+    """One process per GPU: the peer exchange over NVLink (CUDA IPC across
+    devices, st.release.sys / ld.acquire.sys flags) and a real 2-rank NCCL
+    allreduce, both == distributed_solve(2)."""
+    run_ranks(2, "solve", str(tmp_path), 42, 300, 20000, 8, KNEVER, 0.1,
+              env_extra={"UOT_EXCHANGE": exchange, "MR_DEVICE": "rank", "UOT_EXCHANGE_FALLBACK": "0"})
+    _check_solve(tmp_path, orc, 2, 300, 20000, 8, KNEVER, 0.1)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs (gpurun and the round-end box have one)")
+def test_in_process_group_over_distinct_gpus(gpu, orc):
+    """uot_create_group with rank r on GPU r: peer access + direct remote stores
+    across devices, == distributed_solve(P)."""
+    n = min(_ngpus(), 4)
+    a, rpd, cpd = orc.gen_problem(9, 600, 20000)
+    ref = orc.distributed_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, 7, n)
+    res = gpu.distributed_solve(gpu.Problem(a, rpd, cpd, 1.0, 0.1), KNEVER, 7, n, devices=list(range(n)))
+    rel = np.max(np.abs(res.plan.astype(np.float64) - ref.plan) / ref.plan)
+    assert rel <= 1e-5 and res.report.iterations == 7
+    np.testing.assert_allclose(res.factors.beta, ref.beta, rtol=1e-12)
