@@ -72,7 +72,9 @@ typedef struct uot_layout {
   int32_t exchange;      /* 0 single GPU, 1 NCCL allreduce, 2 fused peer-memory exchange */
   int32_t resident;      /* uot_iterate runs as ONE persistent launch, matrix in shared memory (resident.cuh) */
   int32_t dtype;         /* UOT_F32 (Problem<float>) or UOT_F64 (Problem<double>) */
-  int32_t dynamic;       /* 1: row batches handed out by a device counter (uot_set_deterministic) */
+  int32_t dynamic;       /* 1: row batches handed out by a device counter (uot_set_schedule) */
+  int32_t schedule;      /* UOT_SCHEDULE_* of the streaming sweep */
+  int32_t sm_classes;    /* speed classes the class-weighted schedule uses (0: not applicable here) */
   int32_t variant;       /* iteration schedule (UOT_VARIANT_*); rows wider than #SMs slices (G > #SMs,
                             > 1.2M fp32 columns on a B200) run UOT_VARIANT_TWO_PASS, the only one they allow */
 } uot_layout;
@@ -157,14 +159,35 @@ UOT_API int uot_save_problem_file(uot_ctx* ctx, const char* path);
 #define UOT_VARIANT_BASELINE 2
 UOT_API int uot_set_variant(uot_ctx* ctx, int variant);
 
-/* Row-batch schedule of the fused sweep. Default (1): every row group owns a
- * fixed contiguous row block (balanced_blocks, plan.cpp:11-21) and the column
- * partials are reduced in ascending group order: bit-reproducible run to run,
- * as the reference's ordered reduction (fused.hpp:193-196, 242-248). 0: batches
- * go to whichever CTA asks next (a device counter), so SMs with more HBM
- * bandwidth take more rows; the f64 column sums then add rows in a
- * run-dependent order (results agree to ~1e-12 relative between runs). */
+/* Row-batch schedule of the fused sweep. Every row group sums its column
+ * partials in row order and the groups are reduced in ascending order, as the
+ * reference's ordered reduction (fused.hpp:193-196, 242-248); the schedules
+ * differ in which rows a group owns.
+ *   CLASS_WEIGHTED (default): static contiguous row blocks sized by the HBM
+ *     speed class of the group's SMs (B200 SMs stream at three per-TPC rates,
+ *     topology.cuh; the classes are probed once per device and process) —
+ *     bit-reproducible run to run on a given GPU, and balanced.
+ *   UNIFORM: balanced_blocks (plan.cpp:11-21) over the groups — bit-
+ *     reproducible on any GPU, paced by the slowest SMs.
+ *   DYNAMIC: batches go to whichever CTA asks next (a device counter); the
+ *     f64 column sums then add rows in a run-dependent order (results agree to
+ *     ~1e-12 relative between runs).
+ * CLASS_WEIGHTED needs one sweep CTA on every SM; elsewhere it runs UNIFORM. */
+#define UOT_SCHEDULE_CLASS_WEIGHTED 0
+#define UOT_SCHEDULE_UNIFORM 1
+#define UOT_SCHEDULE_DYNAMIC 2
+UOT_API int uot_set_schedule(uot_ctx* ctx, int schedule);
+/* on: UOT_SCHEDULE_CLASS_WEIGHTED; off: UOT_SCHEDULE_DYNAMIC. */
 UOT_API int uot_set_deterministic(uot_ctx* ctx, int on);
+/* Schedule statistics of the last sweep: per CTA slot its SM id and the row
+ * batches it streamed; per row group its class weight (1/32 units). Each output
+ * may be NULL; sizes: grid = groups * G, groups (uot_get_layout). */
+UOT_API int uot_get_schedule_stats(const uot_ctx* ctx, uint32_t* cta_smid, uint32_t* cta_batches,
+                                   uint32_t* group_weight);
+/* The speed class of every SM of `device` (0 = fastest; -1: no crisp classes)
+ * and its probe time in ms (topology.cuh), n entries. Returns UOT_CONFIG_ERROR
+ * when the probe found no crisp classes (the schedule then runs UNIFORM). */
+UOT_API int uot_get_sm_classes(int device, int32_t* cls, double* probe_ms, int n);
 /* Small single-GPU f32 problems whose row blocks fit shared memory run a whole
  * uot_iterate call as ONE cooperative launch (resident.cuh). Default 1; 0 keeps
  * the streaming sweep + finalize per iteration (tests, ablations). */

@@ -61,6 +61,9 @@ struct SweepArgs {
   unsigned int buf_stride;    // bytes per smem ring slot (128-aligned, >= B*slice*4)
   int evict_first;            // stream P past L2 (problem larger than L2)
   int smid_map;               // CTA slot = %smid (the grid covers every SM exactly once)
+  const unsigned* slot_of_sm; // [#SMs] CTA slot of each SM (class-grouped row groups), or nullptr
+  const unsigned long long* gbounds;  // [groups+1] static row block of each group, or nullptr (balanced)
+  unsigned* dbg;              // [grid][2] {smid, batches} of the last sweep (schedule statistics)
   int dyn;                    // batches handed out by a global counter (else a static row block)
   ulonglong2* mail;           // [groups][kMail] {first row, tag}: the group leader's batch picks (dyn, G > 1)
   double fi;
@@ -155,10 +158,13 @@ __device__ __forceinline__ double exchange_row_sum(ulonglong2* xrec, unsigned ct
 // (hardware F2F.F64.F32 runs on the 16/clk/SM conversion pipe, which caps the
 // sweep near the HBM rate: profiles/r01_conv_microbench.txt). Each group of x0
 // values is screened with one VIADDMNMX per value against a per-thread window
-// (ScreenBounds) that certifies x0 AND x1 = f32(f64(x0)*beta_j) positive normal;
-// otherwise the group takes exact hardware conversions. The column sums widen
-// x2 with fastd after a screen of the group's x2 (nn_max), else the hardware
-// conversion. f64 -> f32 is one F2F.F32.F64 (RN), the reference's T(double).
+// (ScreenBounds) that certifies x0 positive normal and x1 = f32(f64(x0)*beta_j)
+// inside [FLT_MIN*2^20, FLT_MAX*2^-20]; otherwise the group takes exact hardware
+// conversions. A row whose factor alpha lies in [2^-20, 2^20] then maps every
+// certified x1 to a positive normal x2 = f32(f64(x1)*alpha), so sweep 2 widens
+// x1 and x2 with fastd and no screen at all; other rows (and rows with an
+// uncertified group) take the hardware conversions. f64 -> f32 is one
+// F2F.F32.F64 (RN), the reference's T(double).
 
 __device__ __forceinline__ uint32_t nn_max(uint32_t m, float x) {
   return max(m, __float_as_uint(x) - 0x800000u);  // >= 0x7f000000 <=> not positive normal
@@ -182,9 +188,12 @@ struct ChunkGroup {
 };
 
 // Screen window of a thread: x0 passes iff lo <= x0 <= hi as floats, with
-// lo = max(FLT_MIN, FLT_MIN/beta_min), hi = min(FLT_MAX, FLT_MAX/beta_max)
-// rounded inward over the thread's beta_j: then x0*beta_j lies in
-// [FLT_MIN, FLT_MAX] exactly, so both rounding steps keep x1 positive normal.
+// lo = max(FLT_MIN, FLT_MIN*M/beta_min), hi = min(FLT_MAX, FLT_MAX/(M*beta_max))
+// rounded inward over the thread's beta_j (M = kAlphaMargin): then x0*beta_j
+// lies in [FLT_MIN*M, FLT_MAX/M] exactly, and both rounding steps keep x1 there
+// (the bounds are representable), so x1*alpha stays positive normal for every
+// alpha in [1/M, M].
+constexpr double kAlphaMargin = 0x1p20;
 struct ScreenBounds {
   uint32_t lo, span;  // bits(lo), bits(hi) - bits(lo)
 };
@@ -200,8 +209,8 @@ __device__ __forceinline__ ScreenBounds screen_bounds(const double* beta, int n)
   }
   if (!(bmax > 0.0)) bmin = bmax = 1.0;
   const double tiny = 1.1754943508222875e-38, big = 3.4028234663852886e38;  // FLT_MIN, FLT_MAX
-  const float lo = __double2float_ru(fmax(tiny, tiny / bmin * (1.0 + 0x1p-40)));
-  const float hi = __double2float_rd(fmin(big, big / bmax * (1.0 - 0x1p-40)));
+  const float lo = __double2float_ru(fmax(tiny, tiny * kAlphaMargin / bmin * (1.0 + 0x1p-40)));
+  const float hi = __double2float_rd(fmin(big, big / (kAlphaMargin * bmax) * (1.0 - 0x1p-40)));
   ScreenBounds b;
   b.lo = __float_as_uint(lo);
   b.span = (bmax < 1e300 && lo <= hi) ? __float_as_uint(hi) - __float_as_uint(lo) : 0u;
@@ -255,9 +264,9 @@ __device__ __forceinline__ void group_sweep1(float4* row, float4 (&v)[KG], uint3
 }
 
 // Sweep 2 of one chunk group (fused.hpp:135-142): x <- f32(f64(x)*alpha) in
-// place, next_j += f64(x). EXACT: x1 may be non-normal (hardware widening).
-// The column sums widen x2 with fastd after a screen of the group (off the
-// 16/clk/SM conversion pipe): +1.3% at 32768^2 over F2F.F64.F32 (measured).
+// place, next_j += f64(x). !EXACT: x1 certified by sweep 1's screen and alpha
+// in [1/M, M], so x1 and x2 are positive normal (fastd both times, +1.3% over
+// the hardware conversion at 32768^2); EXACT: hardware conversions.
 template <int NT, int KG, bool FULL, bool EXACT>
 __device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g0, unsigned tid, unsigned nq,
                                              double al, double* acc) {
@@ -266,25 +275,14 @@ __device__ __forceinline__ void group_sweep2(float4* row, float4 (&w)[KG], int g
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       comp(w[kk], e) = d2f((EXACT ? static_cast<double>(comp(w[kk], e)) : fastd(comp(w[kk], e))) * al);
-  // x2 screened positive normal: widen with integer ops (off the conversion pipe)
-  uint32_t m = 0;
-#pragma unroll
-  for (int kk = 0; kk < KG; ++kk)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) m = nn_max(m, comp(w[kk], e));
-  const bool ok = nn_ok(m);
 #pragma unroll
   for (int kk = 0; kk < KG; ++kk) {
     const unsigned q = tid + (g0 + kk) * NT;
     if (FULL || q < nq) {
       row[q] = w[kk];
-      if (ok) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += fastd(comp(w[kk], e));
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[4 * (g0 + kk) + e] += static_cast<double>(comp(w[kk], e));
-      }
+      for (int e = 0; e < 4; ++e)
+        acc[4 * (g0 + kk) + e] += EXACT ? static_cast<double>(comp(w[kk], e)) : fastd(comp(w[kk], e));
     }
   }
 }
@@ -388,11 +386,13 @@ __device__ __forceinline__ double row_sweep1_tb(float4* row, unsigned tid, unsig
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
 
-// Sweep 2 of this thread's part of one row.
+// Sweep 2 of this thread's part of one row. `exact`: one of the thread's
+// chunk groups of the row took the exact path in sweep 1.
 template <int NT, int V, bool FULL>
 __device__ __forceinline__ void row_sweep2(float4* row, unsigned tid, unsigned nq, double al, bool exact,
                                            double* acc) {
   constexpr int KG = ChunkGroup<V>::KG;
+  exact = exact || !(al >= 1.0 / kAlphaMargin && al <= kAlphaMargin);
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
     float4 w[KG];
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   const unsigned G = a.G;
   // CTA slot: blockIdx, or (smid_map) the SM id, so the G CTAs of a row group
   // sit on neighbouring SMs (same TPC pair / GPC, same die).
-  const unsigned cta = a.smid_map ? smid() : blockIdx.x;
+  const unsigned cta = a.slot_of_sm ? a.slot_of_sm[smid()] : (a.smid_map ? smid() : blockIdx.x);
   const unsigned group = cta / G, g = cta % G;
   // balanced_blocks over groups (plan.cpp:11-21): first rows%groups get one more.
   // Row batches. Static: group `group` owns a contiguous block of rows
@@ -559,8 +559,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   // picks and publishes its pick to the followers through `mail`.
   const unsigned B = a.B;
   const unsigned long long base = a.rows / a.groups, rem = a.rows % a.groups;
-  const unsigned long long r0 = group * base + (group < rem ? group : rem);
-  const unsigned nb_static = static_cast<unsigned>((base + (group < rem ? 1 : 0) + B - 1) / B);
+  // static row block of the group: class-weighted bounds (topology.cuh) or balanced_blocks
+  const unsigned long long r0 = a.gbounds ? a.gbounds[group] : group * base + (group < rem ? group : rem);
+  const unsigned long long r1 = a.gbounds ? a.gbounds[group + 1] : r0 + base + (group < rem ? 1 : 0);
+  const unsigned nb_static = static_cast<unsigned>((r1 - r0 + B - 1) / B);
   const unsigned nq = a.slice / EPC;
   const uint32_t row_bytes = a.slice * static_cast<uint32_t>(sizeof(T));
   T* gbase = static_cast<T*>(a.P) + static_cast<size_t>(g) * a.slice;
@@ -608,9 +610,8 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       // (the seed sweep has no row exchange to bound how far a leader runs
       // ahead of its followers, so with G > 1 it keeps the static blocks)
       if (!a.dyn || (SEED && G > 1)) {
-        const unsigned long long end = r0 + base + (group < rem ? 1 : 0);
         row = b < nb_static ? r0 + static_cast<unsigned long long>(b) * B : kNoRow;
-        if (row != kNoRow) row |= min(static_cast<unsigned long long>(B), end - row) << 56;
+        if (row != kNoRow) row |= min(static_cast<unsigned long long>(B), r1 - row) << 56;
       } else if (G == 1 || g == 0) {
         const unsigned long long t = atomicAdd(&ctl->batch_next, 1ull);
         row = t < nbt ? t * B : kNoRow;
@@ -693,6 +694,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       }
     }
     if (!SEED) bulk_wait<0>();  // every store landed before the CTA retires
+    if (a.dbg) {
+      a.dbg[2 * cta] = smid();
+      a.dbg[2 * cta + 1] = nb;
+    }
 #ifdef UOT_TRACE
     atomicAdd(&uot_trace[8], clock64() - tr_p0);
     TR_FLUSH(4, 5);

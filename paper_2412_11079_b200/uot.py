@@ -90,7 +90,8 @@ class Layout(C.Structure):
                 ("nranks", C.c_int32), ("device", C.c_int32), ("evict_first", C.c_int32),
                 ("smid_map", C.c_int32), ("exchange", C.c_int32),
                 ("resident", C.c_int32), ("dtype", C.c_int32),
-                ("dynamic", C.c_int32), ("variant", C.c_int32)]
+                ("dynamic", C.c_int32), ("schedule", C.c_int32), ("sm_classes", C.c_int32),
+                ("variant", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -129,6 +130,9 @@ def lib():
     L.uot_set_variant.argtypes = [_P, _i]
     L.uot_set_deterministic.argtypes = [_P, _i]
     L.uot_set_resident.argtypes = [_P, _i]
+    L.uot_set_schedule.argtypes = [_P, _i]
+    L.uot_get_schedule_stats.argtypes = [_P, _P, _P, _P]
+    L.uot_get_sm_classes.argtypes = [_i, _P, _P, _i]
     L.uot_problem_file_info.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_i),
                                         C.POINTER(_d), C.POINTER(_d)]
     L.uot_last_io_error.restype = C.c_char_p
@@ -582,19 +586,42 @@ class Session:
             _raise(1, f"unknown iteration variant {name!r}")
         self._check(lib().uot_set_variant(self._h, self.VARIANTS[name]))
 
+    SCHEDULES = {"class_weighted": 0, "uniform": 1, "dynamic": 2}
+
+    def set_schedule(self, name: str):
+        """Row-batch schedule of the sweep (uot_set_schedule): "class_weighted"
+        (default; static row blocks sized by the SMs' HBM speed class,
+        bit-reproducible), "uniform" (balanced_blocks) or "dynamic"."""
+        if name not in self.SCHEDULES:
+            _raise(1, f"unknown schedule {name!r}")
+        self._check(lib().uot_set_schedule(self._h, self.SCHEDULES[name]))
+        self._refresh_layout()
+
     def set_deterministic(self, on: bool = True):
-        """Fixed row blocks per CTA group (the default: bit-reproducible run to
-        run), or with on=False the dynamic batch counter (uot_set_deterministic)."""
+        """on: the class-weighted static schedule (default, bit-reproducible run
+        to run); off: the dynamic batch counter (uot_set_deterministic)."""
         self._check(lib().uot_set_deterministic(self._h, 1 if on else 0))
-        self.layout["dynamic"] = 0 if on else 1
+        self._refresh_layout()
+
+    def _refresh_layout(self):
+        lay = Layout()
+        lib().uot_get_layout(self._h, C.byref(lay))
+        self.layout = lay.as_dict()
+
+    def schedule_stats(self):
+        """Per CTA slot: SM id and row batches of the last sweep; per group: class weight (1/32)."""
+        grid = self.layout["groups"] * self.layout["G"]
+        smid = np.zeros(grid, np.uint32)
+        nb = np.zeros(grid, np.uint32)
+        w = np.zeros(self.layout["groups"], np.uint32)
+        self._check(lib().uot_get_schedule_stats(self._h, _ptr(smid), _ptr(nb), _ptr(w)))
+        return smid, nb, w
 
     def set_resident(self, on: bool = True):
         """Allow (default) or forbid the one-launch resident solve for small
         problems (uot_set_resident)."""
         self._check(lib().uot_set_resident(self._h, 1 if on else 0))
-        lay = Layout()
-        lib().uot_get_layout(self._h, C.byref(lay))
-        self.layout = lay.as_dict()
+        self._refresh_layout()
 
     def set_timing(self, on: bool = True):
         self._check(lib().uot_set_timing(self._h, 1 if on else 0))
@@ -779,3 +806,16 @@ def _cached_session(m: int, n: int, device: int, dtype=np.float32) -> "Session":
             s.close()
         _tls.session, _tls.key = Session(m, n, device, dtype=dtype), key
     return _tls.session
+
+
+def sm_classes(device: int = 0):
+    """(class per SM, probe ms per SM) of `device` (topology.cuh); class -1
+    everywhere when the probe found no crisp speed classes."""
+    n = 1024
+    cls = np.full(n, -1, np.int32)
+    ms = np.zeros(n, np.float64)
+    rc = lib().uot_get_sm_classes(int(device), _ptr(cls), _ptr(ms), n)
+    if rc not in (0, 4):
+        _raise(rc, "uot_get_sm_classes failed")
+    k = int(np.count_nonzero(ms))
+    return cls[:k], ms[:k]

@@ -52,10 +52,33 @@ def test_library_is_sm100a_code(uot):
     assert "sm_100a" in out
 
 
-def test_sweep_uses_bulk_copies_and_mbarriers(uot):
-    sass = subprocess.run(["cuobjdump", "-sass", uot._build.SO], capture_output=True, text=True).stdout
-    assert "UBLKCP" in sass  # cp.async.bulk (TMA engine) loads and stores
-    assert "SYNCS" in sass   # mbarrier pipeline
+HEADLINE = "_ZN4uotk12sweep_kernelILi512ELi4ELi1ELi7ELi2ELb1ELi2ELb1ELb0EfLb1EEEvNS_9SweepArgsE"
+
+
+def headline_sass(so):
+    """SASS of the 32768^2 sweep instance (512 compute threads, 4 float4 per
+    thread, G > 1 exchange, full slices, column factors in TMEM)."""
+    out = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    blocks = out.split("Function : ")
+    return next(b for b in blocks if b.startswith(HEADLINE))
+
+
+def test_sweep_uses_bulk_copies_mbarriers_and_tmem(uot):
+    sass = headline_sass(uot._build.SO)
+    assert "UBLKCP" in sass   # cp.async.bulk (TMA engine) loads and stores
+    assert "SYNCS" in sass    # mbarrier pipeline
+    assert "LDTM" in sass and "STTM" in sass  # column factors parked in / read from Tensor Memory
+    assert "F2F.F32.F64" in sass and "DMUL" in sass  # the reference's f64 product rounded to f32
+
+
+def test_headline_sweep_does_not_spill():
+    log = os.path.join(ROOT, "paper_2412_11079_b200", "build.log")
+    if not os.path.exists(log):
+        pytest.skip("build.log not present (library built elsewhere)")
+    text = open(log).read()
+    i = text.index(f"Function properties for {HEADLINE}")
+    props = text[i:i + 400]
+    assert "0 bytes spill stores, 0 bytes spill loads" in props
 
 
 def test_host_scalars_match_reference(uot, orc):

@@ -10,8 +10,8 @@ er = 1, ep = 0.1).
 * config 5 (131072 x 32768, row-sharded, K = 20): the in-process rank group
   (uot_create_group, distributed_solve's own call shape, distributed.hpp:52-142)
   with 2 and 4 ranks — on distinct GPUs when the box has them, else sharing
-  GPU 0 — against the reference's W-worker iteration, which is bitwise its
-  distributed_solve(W) (test_distributed.cpp:106-118).
+  GPU 0 — against the reference's W-worker iteration at W = nproc (its
+  distributed_solve(W) is bitwise the same, test_distributed.cpp:106-118).
 
 The GPU generates the problem in HBM (bit-identical to gen_problem_t, tested in
 test_gpu_parity.py) and the plans are compared block by block, so the host
@@ -93,13 +93,13 @@ def test_baseline_config_full_k_vs_reference(gpu, orc, ref, cfg, m, n, k):
 
 def _devices(ranks):
     import torch
-    n = torch.cuda.device_count() if torch.cuda.is_available() else 1
-    return [r % n for r in range(ranks)] if n >= ranks else [0] * ranks
+    n = max(1, torch.cuda.device_count() if torch.cuda.is_available() else 1)
+    return [r % n for r in range(ranks)]
 
 
 def test_config5_row_sharded_ranks_vs_reference(gpu, orc, ref):
     m, n, k = 131072, 32768, 20
-    r, rpd, cpd = reference_run(ref, orc, m, n, k, 4)  # == the reference's distributed_solve(4)
+    r, rpd, cpd = reference_run(ref, orc, m, n, k, THREADS)  # == the reference's distributed_solve(THREADS)
     for ranks in (2, 4):
         with gpu.SessionGroup(m, n, ranks, devices=_devices(ranks)) as g:
             for s in g.ranks:
@@ -115,6 +115,7 @@ def test_config5_row_sharded_ranks_vs_reference(gpu, orc, ref):
                 alpha[b:b + s.rows] = f.alpha
                 cmp.block(b, s.plan())
                 np.testing.assert_allclose(f.beta, r.beta, rtol=1e-9)
-        cmp.check(f"config 5 {m}x{n} K={k} as {ranks} ranks on devices {_devices(ranks)} vs the reference (W=4)")
+        cmp.check(f"config 5 {m}x{n} K={k} as {ranks} ranks on devices {_devices(ranks)} vs the reference "
+                  f"(W={THREADS})")
         np.testing.assert_allclose(alpha, r.alpha, rtol=1e-9)
         assert abs(err - r.final_error) <= TOL * r.final_error

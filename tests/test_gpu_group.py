@@ -122,6 +122,18 @@ def test_group_collectives_reject_ranks_of_different_groups(gpu):
     uot = gpu
     with uot.SessionGroup(40, 300, 2, devices=[0, 0]) as g1, uot.SessionGroup(40, 300, 2, devices=[0, 0]) as g2:
         import ctypes as C
+        # every rank has a problem, so only the group check can refuse the call
+        # (without it rank 1 of g2 would wait for a peer of g1 that never publishes)
+        for g in (g1, g2):
+            for s in g.ranks:
+                s.generate_problem(3, 1.0, 0.1)
         mixed = (C.c_void_p * 2)(g1.ranks[0]._h.value, g2.ranks[1]._h.value)
         rc = uot.lib().uot_group_init_col_sums(C.cast(mixed, C.c_void_p), 2)
         assert rc == 1  # UOT_INVALID_PARAMETER, no hang on a peer that never publishes
+        assert "session group" in g2.ranks[1]._err()
+        it, err, conv = C.c_uint64(), C.c_double(), C.c_int()
+        rc = uot.lib().uot_group_iterate(C.cast(mixed, C.c_void_p), 2, 3, 1e-300, C.byref(it), C.byref(err),
+                                         C.byref(conv))
+        assert rc == 1 and "session group" in g2.ranks[1]._err()
+        g1.init_col_sums()  # the groups themselves still work
+        assert g1.iterate(2)[0] == 2

@@ -396,3 +396,29 @@ def test_concurrent_sessions_in_threads(gpu, orc):
         for seed, (g, r) in out.items():
             rel = np.max(np.abs(g.plan.astype(np.float64) - r.plan) / r.plan)
             assert rel <= 1e-5 and g.report.iterations == r.iterations, (seed, rel)
+
+
+def test_set_col_sums_after_convergence(gpu, orc):
+    """A converged session given a new FusedState (uot_set_col_sums) runs again:
+    beta is recomputed from the caller's sums and the next iteration equals the
+    reference's fused_iterate from that state (fused.hpp:164-191)."""
+    a, rpd, cpd = orc.gen_problem(37, 48, 64)
+    cpd = cpd * (rpd.sum() / cpd.sum())
+    with gpu.Session(48, 64) as s:
+        s.set_problem(gpu.Problem(a, rpd, cpd, 1.0, 0.0))
+        s.init_col_sums()
+        it, err, conv = s.iterate(10000, 1e-6)
+        assert conv
+        plan = s.plan()
+        cs = orc.init_col_sums(plan)  # a different (exact seed) state than the carried one
+        s.set_col_sums(cs)
+        it2, err2, conv2 = s.iterate(1, 1e-300)
+        assert it2 == 1
+        got = s.plan()
+        f = s.factors()
+    ref_plan = plan.copy()
+    ref_cs = cs.copy()
+    fi = orc.compute_fi(1.0, 0.0)
+    _, rbeta = orc.fused_iterate(ref_plan, ref_cs, rpd, cpd, fi, 1)
+    np.testing.assert_allclose(f.beta, rbeta, rtol=1e-14)
+    assert_parity(got, ref_plan, rpd, cpd, "after set_col_sums")
