@@ -298,6 +298,20 @@ def run_ours(args, grp: Group):
     # ---- device-resident throughput (the `value`) -------------------------
     s.generate_problem(SEED, ER, EP)  # gen_problem_t bits, generated in HBM
     s.init_col_sums()
+    # The deterministic weighted schedule (uot_set_schedule): row blocks sized
+    # by per-row-group weights measured once (uot_calibrate_schedule: 4
+    # dynamic iterations on a scratch copy of the plan, untimed); every solve
+    # with these weights is bit-reproducible. Falls back to the uniform blocks
+    # where the sweep does not run one CTA on every SM.
+    weights = None
+    schedule = args.schedule
+    if schedule == "weighted":
+        if s.layout["pinned"]:
+            weights = s.calibrate_schedule(4)
+        else:
+            schedule = "uniform"
+    s.set_schedule(schedule)
+    lay = s.layout
     s.iterate(args.warmup, KNEVER)
     s.set_timing(True)
     launches0 = s.kernel_launches()
@@ -326,6 +340,19 @@ def run_ours(args, grp: Group):
     peak, peak_src = peak_hbm()
     achieved = bytes_iter_local / (sweep_avg_ms / 1e3) / 1e9
 
+    # ---- the other row-batch schedules, same steps (transparency) -----------
+    schedules = {schedule: value}
+    if not args.no_schedule_ab:
+        for other in ("uniform", "weighted", "dynamic"):
+            if other in schedules or (other == "weighted" and weights is None):
+                continue
+            s.set_schedule(other)
+            s.iterate(args.warmup, KNEVER)
+            grp.barrier()
+            _, _, _, ms_o = s.iterate_timed(args.steps, KNEVER)
+            schedules[other] = units * args.steps / (grp.max(ms_o) / 1e3)
+        s.set_schedule(schedule)
+
     # ---- sustained: >= args.sustained_s of back-to-back iterations ---------
     sustained = None
     if args.sustained_s > 0:
@@ -352,23 +379,30 @@ def run_ours(args, grp: Group):
         out = uot.PinnedBuffer((rows_local, COLS), np.float32)
         grp.barrier()
         t0 = time.perf_counter()
+        phases = {}
         if world > 1:
             res = D.distributed_solve(p, KNEVER, args.steps, session=s, global_rows=rows_global)
             it2 = res.report.iterations
             out.array[...] = res.plan
         else:
             s.set_problem(p)              # H2D of A, rpd, cpd + validation (problem.hpp:64-103)
+            t1 = time.perf_counter()
             s.init_col_sums()
             it2, _, _ = s.iterate(args.steps, KNEVER)
+            t2 = time.perf_counter()
             s.factors()                    # D2H alpha, beta
             s.plan(out=out.array)          # D2H plan
+            t3 = time.perf_counter()
+            phases = {"upload_validate_ms": (t1 - t0) * 1e3, "seed_iterate_ms": (t2 - t1) * 1e3,
+                      "download_ms": (t3 - t2) * 1e3,
+                      "h2d_gbs": (rows_local * COLS * 4) / (t1 - t0) / 1e9,
+                      "d2h_gbs": (rows_local * COLS * 4) / (t3 - t2) / 1e9}
         wall = grp.max(time.perf_counter() - t0)
         h2d = rows_local * COLS * 4 + rows_local * 8 + COLS * 8
         d2h = rows_local * COLS * 4 + rows_local * 8 + COLS * 8
         e2e = {"value": units * it2 / wall, "unit": UNIT,
                "h2d_bytes_per_step": h2d * world / args.steps, "d2h_bytes_per_step": d2h * world / args.steps,
-               "wall_ms": wall * 1e3,
-               "pcie_gbs_if_serial": (h2d + d2h) / max(wall - max_ms / 1e3, 1e-9) / 1e9,
+               "wall_ms": wall * 1e3, **phases,
                "what": (f"fused_solve through the C ABI from page-locked host buffers: upload + validate "
                         f"{rows_local}x{COLS} per rank, init_col_sums, {args.steps} iterations, download "
                         f"plan + factors; wall {wall * 1e3:.1f} ms (max over ranks); per-step bytes = run bytes / steps")}
@@ -396,12 +430,15 @@ def run_ours(args, grp: Group):
             "rows_global": rows_global, "cols": COLS, "rows_per_gpu": rows_local, "storage": "f32",
             "arithmetic": "f64 products rounded once to f32, f64 sums (bit-compatible with the reference)",
             "parallelism": f"row-sharded x{world}" + xdesc,
-            "schedule": "fixed row blocks (deterministic, bit-reproducible run to run)" if not lay["dynamic"]
-                        else "dynamic row batches",
+            "schedule": {"weighted": "weighted static row blocks (weights calibrated once, untimed; "
+                                     "deterministic: bit-reproducible for the given weights)",
+                         "uniform": "uniform static row blocks, balanced_blocks (the default; bit-reproducible)",
+                         "dynamic": "dynamic row batches (device counter; ~1e-12 run-to-run differences)"}[schedule],
             "l2": f"no flush: the resident matrix ({bytes_iter_local / 2 / 2**30:.1f} GiB/GPU) exceeds the 126 MB L2",
             "layout": {k: lay[k] for k in ("G", "groups", "slice", "threads", "nbuf", "rows_per_step", "smem_bytes",
-                                           "dynamic")},
+                                           "dynamic", "schedule", "pinned")},
         },
+        "schedules_value": schedules,
         "hbm_gbs": hbm_gbs,
         # the metric's own yardstick (report both): nominal 8 TB/s per GPU, and the measured copy peak
         "hbm_frac_of_8tbs": hbm_gbs / (8000.0 * world),
@@ -463,6 +500,9 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=0, help="cpu_baseline timed iterations (default: --steps)")
     ap.add_argument("--cpu-w1-iters", type=int, default=2, help="cpu_baseline W=1 iterations (0: skip)")
     ap.add_argument("--rows", type=int, default=0, help=argparse.SUPPRESS)  # tests: small stand-in workload
+    ap.add_argument("--schedule", choices=["weighted", "uniform", "dynamic"], default="weighted",
+                    help="row-batch schedule of the timed region (default: weighted, deterministic)")
+    ap.add_argument("--no-schedule-ab", action="store_true", help="skip timing the other two schedules")
     ap.add_argument("--sustained-s", type=float, default=2.0,
                     help="seconds of back-to-back iterations for the `sustained` block (0: skip)")
     args = ap.parse_args()

@@ -74,7 +74,7 @@ typedef struct uot_layout {
   int32_t dtype;         /* UOT_F32 (Problem<float>) or UOT_F64 (Problem<double>) */
   int32_t dynamic;       /* 1: row batches handed out by a device counter (uot_set_schedule) */
   int32_t schedule;      /* UOT_SCHEDULE_* of the streaming sweep */
-  int32_t sm_classes;    /* speed classes the class-weighted schedule uses (0: not applicable here) */
+  int32_t pinned;        /* one sweep CTA on every SM, slot = SM id (the weighted schedule is available) */
   int32_t variant;       /* iteration schedule (UOT_VARIANT_*); rows wider than #SMs slices (G > #SMs,
                             > 1.2M fp32 columns on a B200) run UOT_VARIANT_TWO_PASS, the only one they allow */
 } uot_layout;
@@ -163,31 +163,39 @@ UOT_API int uot_set_variant(uot_ctx* ctx, int variant);
  * partials in row order and the groups are reduced in ascending order, as the
  * reference's ordered reduction (fused.hpp:193-196, 242-248); the schedules
  * differ in which rows a group owns.
- *   CLASS_WEIGHTED (default): static contiguous row blocks sized by the HBM
- *     speed class of the group's SMs (B200 SMs stream at three per-TPC rates,
- *     topology.cuh; the classes are probed once per device and process) —
- *     bit-reproducible run to run on a given GPU, and balanced.
- *   UNIFORM: balanced_blocks (plan.cpp:11-21) over the groups — bit-
- *     reproducible on any GPU, paced by the slowest SMs.
+ *   UNIFORM (default): balanced_blocks (plan.cpp:11-21) over the groups —
+ *     bit-reproducible run to run on any GPU; paced by the slowest SMs (B200
+ *     SMs stream HBM at per-TPC rates that differ by up to 1.6x).
+ *   WEIGHTED: static contiguous row blocks proportional to per-group weights
+ *     (uot_set_group_weights, or measured by uot_calibrate_schedule); CTA slots
+ *     are pinned to SMs, so the weights stay attached to the SMs they describe —
+ *     bit-reproducible for given weights, and balanced.
  *   DYNAMIC: batches go to whichever CTA asks next (a device counter); the
  *     f64 column sums then add rows in a run-dependent order (results agree to
  *     ~1e-12 relative between runs).
- * CLASS_WEIGHTED needs one sweep CTA on every SM; elsewhere it runs UNIFORM. */
-#define UOT_SCHEDULE_CLASS_WEIGHTED 0
-#define UOT_SCHEDULE_UNIFORM 1
+ * WEIGHTED needs one sweep CTA on every SM (uot_layout.pinned). */
+#define UOT_SCHEDULE_UNIFORM 0
+#define UOT_SCHEDULE_WEIGHTED 1
 #define UOT_SCHEDULE_DYNAMIC 2
 UOT_API int uot_set_schedule(uot_ctx* ctx, int schedule);
-/* on: UOT_SCHEDULE_CLASS_WEIGHTED; off: UOT_SCHEDULE_DYNAMIC. */
+/* on: WEIGHTED when weights are set, else UNIFORM; off: DYNAMIC. */
 UOT_API int uot_set_deterministic(uot_ctx* ctx, int on);
+/* Weights (1 .. 2^20) of the `n` = uot_layout.groups row groups, group g = CTA
+ * slots g*G .. g*G+G-1 = SMs g*G .. ; selects WEIGHTED. */
+UOT_API int uot_set_group_weights(uot_ctx* ctx, const uint32_t* weights, uint32_t n);
+UOT_API int uot_get_group_weights(const uot_ctx* ctx, uint32_t* weights, uint32_t n);
+/* Measure the weights: k dynamic iterations (k in [2, 64], the first
+ * discarded) of the fused sweep on a scratch copy of the plan; each group's
+ * weight is the row batches it took. The session's plan, factors, column sums
+ * and stop state are unchanged. Needs a problem and init_col_sums; selects
+ * WEIGHTED. Store the weights (uot_get_group_weights) to reuse them across
+ * sessions and processes on the same GPU. */
+UOT_API int uot_calibrate_schedule(uot_ctx* ctx, uint32_t k);
 /* Schedule statistics of the last sweep: per CTA slot its SM id and the row
- * batches it streamed; per row group its class weight (1/32 units). Each output
- * may be NULL; sizes: grid = groups * G, groups (uot_get_layout). */
+ * batches it streamed; per row group its weight (1 when none are set). Each
+ * output may be NULL; sizes: grid = groups * G, groups (uot_get_layout). */
 UOT_API int uot_get_schedule_stats(const uot_ctx* ctx, uint32_t* cta_smid, uint32_t* cta_batches,
                                    uint32_t* group_weight);
-/* The speed class of every SM of `device` (0 = fastest; -1: no crisp classes)
- * and its probe time in ms (topology.cuh), n entries. Returns UOT_CONFIG_ERROR
- * when the probe found no crisp classes (the schedule then runs UNIFORM). */
-UOT_API int uot_get_sm_classes(int device, int32_t* cls, double* probe_ms, int n);
 /* Small single-GPU f32 problems whose row blocks fit shared memory run a whole
  * uot_iterate call as ONE cooperative launch (resident.cuh). Default 1; 0 keeps
  * the streaming sweep + finalize per iteration (tests, ablations). */

@@ -96,6 +96,27 @@ __global__ void reset_control_kernel(Control* c) {
   c->batch_next = 0;
 }
 
+// Undo a calibration run (uot_calibrate_schedule): the per-problem fields come
+// back from `saved`; the never-reset tags (epoch, xseq, sweep_seq) keep moving
+// forward so no stale exchange record or mailbox entry can match again.
+__global__ void restore_control_kernel(Control* c, const Control* saved) {
+  c->iter = saved->iter;
+  c->allreduce_calls = saved->allreduce_calls;
+  c->doubles_reduced = saved->doubles_reduced;
+  c->tol = saved->tol;
+  c->last_error = saved->last_error;
+  c->err_beta[0] = saved->err_beta[0];
+  c->err_beta[1] = saved->err_beta[1];
+  c->done = saved->done;
+  c->converged = saved->converged;
+  c->status = saved->status;
+  c->beta_bad = saved->beta_bad;
+  c->beta_bad_next = saved->beta_bad_next;
+  c->alpha_bad = saved->alpha_bad;
+  c->fin_count = 0;
+  c->batch_next = 0;
+}
+
 // A caller-supplied FusedState (uot_set_col_sums): a converged session may run
 // again; a failed one stays stopped.
 __global__ void resume_control_kernel(Control* c) {

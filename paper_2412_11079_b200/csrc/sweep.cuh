@@ -96,7 +96,7 @@ __host__ __device__ constexpr int tr_slot(int id) {
 #endif
 
 constexpr int kRing = 8;   // exchange records per CTA
-constexpr int kQ = 4;      // ring depth of row partials / factors handed between roles
+constexpr int kQ = 4;      // ring depth of row partials / factors handed between roles (>= LA + 2)
 constexpr int kMail = 32;  // batch picks a group leader publishes ahead of its followers
 constexpr unsigned long long kNoRow = ~0ull;  // ring slot sentinel: no batch left
 
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   constexpr int kTbCols = (8 * V * (NW / 4) <= 32) ? 32 : (8 * V * (NW / 4) <= 64) ? 64 : (8 * V * (NW / 4) <= 128) ? 128 : 256;
   constexpr int EPC = elems_per_chunk<T>();  // 4 floats or 2 doubles per 16-byte chunk
   static_assert(NF >= 1 && NF <= kErrSlots, "factor warps");
-  static_assert(LA >= 1 && LA <= 2 && (!XCHG || LA == 2), "lag (the alpha / red rings hold kQ batches)");
+  static_assert(LA >= 1 && LA + 2 <= kQ && (!XCHG || LA >= 2), "lag (the alpha / red rings hold kQ batches)");
   static_assert(NBUF >= LA + 4, "ring too small");
   static_assert(!XCHG || BM == 1, "the exchange path moves one row per batch");
 

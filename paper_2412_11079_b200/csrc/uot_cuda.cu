@@ -26,7 +26,6 @@
 #include "problem.cuh"
 #include "sweep.cuh"
 #include "resident.cuh"
-#include "topology.cuh"
 #include "ablation.cuh"
 
 using namespace uotk;
@@ -50,7 +49,10 @@ struct SweepCfg {
 // pow and, for G > 1, the L2 exchange round trip). Factor warps alternate
 // batches: 3 for G == 1, 2 when G > 1 (measured: more warps polling L2 cost
 // more issue slots than they buy).
+// (Measured: a lag of 3 for G > 1 — more slack between a group's CTAs — is
+// 10-15% slower: the 7-slot ring then prefetches only two batches.)
 constexpr int kLag = 2;
+constexpr int kLagX = 2;
 constexpr int kFactorWarpsG1 = 3;
 constexpr int kFactorWarpsX = 2;
 // Column factors of sweep 1 parked in TMEM (sweep.cuh, TB) for slices of 3-4
@@ -67,8 +69,9 @@ SweepCfg make_cfg() {
   c.nf = NF;
   c.xchg = XCHG;
   constexpr bool TB = V >= 3;
-  c.iter[0] = sweep_kernel<NT, V, BM, NB, kLag, XCHG, NF, false, false, float, TB>;
-  c.iter[1] = sweep_kernel<NT, V, BM, NB, kLag, XCHG, NF, true, false, float, TB>;
+  constexpr int LA = XCHG ? kLagX : kLag;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false, float, TB>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false, float, TB>;
   c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true>;
   c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
@@ -110,8 +113,9 @@ SweepCfg make_cfg_f64() {
   c.nbuf = NB;
   c.nf = NF;
   c.xchg = XCHG;
-  c.iter[0] = sweep_kernel<NT, V, BM, NB, kLag, XCHG, NF, false, false, double>;
-  c.iter[1] = sweep_kernel<NT, V, BM, NB, kLag, XCHG, NF, true, false, double>;
+  constexpr int LA = XCHG ? kLagX : kLag;
+  c.iter[0] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, false, false, double>;
+  c.iter[1] = sweep_kernel<NT, V, BM, NB, LA, XCHG, NF, true, false, double>;
   c.seed[0] = sweep_kernel<NT, V, BM, NB, 1, false, 1, false, true, double>;
   c.seed[1] = sweep_kernel<NT, V, BM, NB, 1, false, 1, true, true, double>;
   c.smem_bytes = &SweepSmem<NT / 32, BM, NB>::bytes;
@@ -192,123 +196,6 @@ struct Status {
   std::string msg;
 };
 
-// ---------------------------------------------------- SM speed classes --
-// topology.cuh: per-SM in-place streaming time under full load, probed once per
-// device and process, clustered into classes at gaps of > 8% between sorted
-// times (B200: three classes 0.82 / 1.18 / 1.33 ms, +-1%, per TPC).
-struct SmClasses {
-  bool ok = false;
-  std::string why;
-  std::vector<double> ms;        // probe time per smid
-  std::vector<int> cls;          // class per smid, 0 = fastest
-  std::vector<double> class_ms;  // median probe time per class
-};
-
-int probe_sm_times(int device, std::vector<double>* ms, std::string* why) {
-  int sms = 0;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 1;
-  constexpr unsigned nb = 48;  // 1.5 MiB per SM: 227 MB in all, past L2
-  unsigned char* buf = nullptr;
-  unsigned long long* out = nullptr;
-  cudaStream_t st = nullptr;
-  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&buf, static_cast<size_t>(sms) * nb * kProbeBytes);
-  if (e == cudaSuccess) e = cudaMalloc(&out, sizeof(unsigned long long) * sms);
-  if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, static_cast<size_t>(sms) * nb * kProbeBytes, st);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(sm_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sm_probe_smem()));
-  std::vector<std::vector<double>> reps(static_cast<size_t>(sms));
-  for (int r = 0; r < 4 && e == cudaSuccess; ++r) {
-    e = cudaMemsetAsync(out, 0xff, sizeof(unsigned long long) * sms, st);
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(sms);
-    lc.blockDim = dim3(32);
-    lc.dynamicSmemBytes = sm_probe_smem();
-    lc.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: one per SM
-    at[0].val.cooperative = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    if (e == cudaSuccess) e = cudaLaunchKernelEx(&lc, sm_probe_kernel, buf, nb, out);
-    std::vector<unsigned long long> h(sms);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), out, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (r == 0) continue;  // warm-up
-    for (int i = 0; i < sms && e == cudaSuccess; ++i) reps[i].push_back(static_cast<double>(h[i]) * 1e-6);
-  }
-  if (buf) cudaFree(buf);
-  if (out) cudaFree(out);
-  if (st) cudaStreamDestroy(st);
-  if (e != cudaSuccess) {
-    *why = std::string("probe: ") + cudaGetErrorString(e);
-    cudaGetLastError();
-    return 1;
-  }
-  ms->assign(sms, 0.0);
-  for (int i = 0; i < sms; ++i) {
-    std::sort(reps[i].begin(), reps[i].end());
-    (*ms)[i] = reps[i][reps[i].size() / 2];
-  }
-  return 0;
-}
-
-// Cluster sorted per-SM times at relative gaps > 8%: crisp classes or nothing.
-void classify(SmClasses* c) {
-  const int n = static_cast<int>(c->ms.size());
-  std::vector<int> idx(n);
-  for (int i = 0; i < n; ++i) idx[i] = i;
-  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return c->ms[a] < c->ms[b]; });
-  c->cls.assign(n, 0);
-  std::vector<std::vector<double>> members(1);
-  for (int k = 0; k < n; ++k) {
-    const double t = c->ms[idx[k]];
-    if (!(t > 0.0) || t > 1e6) {
-      c->why = "an SM reported no probe time";
-      return;
-    }
-    if (k > 0 && t > c->ms[idx[k - 1]] * 1.08) members.emplace_back();
-    c->cls[idx[k]] = static_cast<int>(members.size()) - 1;
-    members.back().push_back(t);
-  }
-  if (members.size() > 6) {
-    c->why = "no crisp speed classes";
-    return;
-  }
-  for (auto& m : members) {
-    // a class must not straddle a noise gradient: its spread stays within 5%
-    if (m.back() > m.front() * 1.05) {
-      c->why = "a speed class spreads over more than 5%";
-      return;
-    }
-    c->class_ms.push_back(m[m.size() / 2]);
-  }
-  c->ok = true;
-}
-
-std::mutex g_classes_mu;
-std::map<int, SmClasses> g_classes;
-
-const SmClasses& sm_classes(int device) {
-  std::lock_guard<std::mutex> lk(g_classes_mu);
-  auto it = g_classes.find(device);
-  if (it != g_classes.end()) return it->second;
-  SmClasses c;
-  if (probe_sm_times(device, &c.ms, &c.why) == 0) classify(&c);
-  return g_classes.emplace(device, std::move(c)).first->second;
-}
-
-// Relative speed of a class in the fused sweep (slowest class = 1), in 1/32
-// units: the probe's streaming ratio, capped where the sweep's per-SM compute
-// rather than its HBM share bounds the faster SMs.
-constexpr double kClassCap = 1.5;
-unsigned class_weight(const SmClasses& c, int k) {
-  const double slowest = c.class_ms.back();
-  const double r = std::min(kClassCap, slowest / c.class_ms[static_cast<size_t>(k)]);
-  return static_cast<unsigned>(std::lround(std::max(1.0, r) * 32.0));
-}
-
 }  // namespace
 
 struct uot_ctx {
@@ -339,15 +226,12 @@ struct uot_ctx {
   int full = 0;
   int smid_map = 0;
   int dyn = 1;  // batches handed out by a global counter (SweepArgs::dyn)
-  int schedule = UOT_SCHEDULE_CLASS_WEIGHTED;  // uot_set_schedule
-  bool class_ok = false;           // slot_of_sm / gbounds built (one CTA per SM, crisp classes)
-  int nclasses = 0;
-  unsigned* d_slot = nullptr;       // [sms] CTA slot of each SM (row groups of one speed class)
-  unsigned long long* d_gbounds = nullptr;  // [groups+1] class-weighted static row blocks
+  int schedule = UOT_SCHEDULE_UNIFORM;  // uot_set_schedule
+  bool pinned = false;              // one sweep CTA on every SM: CTA slot = %smid (d_slot)
+  unsigned* d_slot = nullptr;       // [sms] CTA slot of each SM (identity)
+  unsigned long long* d_gbounds = nullptr;  // [groups+1] weighted static row blocks (UOT_SCHEDULE_WEIGHTED)
   unsigned* d_dbg = nullptr;        // [grid][2] {smid, batches} of the last sweep
-  std::vector<unsigned> class_w;   // per group weight (1/32 units)
-  std::vector<unsigned> h_slot;    // host copies of the two tables
-  std::vector<unsigned long long> h_gbounds;
+  std::vector<uint32_t> weights;    // per row group (UOT_SCHEDULE_WEIGHTED)
   ulonglong2* mail = nullptr;  // [groups][kMail] batch picks of the group leaders
   // resident mode: the whole uot_iterate call is one persistent launch
   const ResidentCfg* rcfg = nullptr;
@@ -436,58 +320,27 @@ int probe_smid_map(uot_ctx* ctx) {
   return UOT_OK;
 }
 
-// Class-weighted static schedule (topology.cuh): when the sweep runs one CTA on
-// every SM, row group k is made of G SMs of ONE speed class (slots assigned in
-// (class, smid) order; SMs left over by class sizes not divisible by G form
-// the last groups, weighted by their slowest member) and owns a contiguous
-// row block proportional to its class weight. Deterministic on a given GPU:
-// the same classes give the same slots and bounds every run.
-void plan_class_schedule(uot_ctx* ctx, int smem_optin) {
-  ctx->class_ok = false;
-  ctx->nclasses = 0;
-  // one CTA per SM: the grid covers every SM and two CTAs cannot share one
-  if (ctx->grid != static_cast<unsigned>(ctx->sms) || 2 * ctx->smem <= static_cast<size_t>(smem_optin) + 1024)
-    return;
-  const SmClasses& c = sm_classes(ctx->device);
-  if (!c.ok || static_cast<int>(c.cls.size()) != ctx->sms) return;
-  const unsigned G = ctx->G, groups = ctx->groups;
-  std::vector<int> order(ctx->sms);
-  for (int i = 0; i < ctx->sms; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return c.cls[a] < c.cls[b]; });
-  // whole groups inside each class first, leftovers (mixed classes) last
-  std::vector<int> whole, left;
-  for (size_t k = 0; k < order.size();) {
-    size_t e = k;
-    while (e < order.size() && c.cls[order[e]] == c.cls[order[k]]) ++e;
-    const size_t full = (e - k) / G * G;
-    for (size_t i = k; i < k + full; ++i) whole.push_back(order[i]);
-    for (size_t i = k + full; i < e; ++i) left.push_back(order[i]);
-    k = e;
-  }
-  whole.insert(whole.end(), left.begin(), left.end());
-  ctx->h_slot.assign(ctx->sms, 0);
-  ctx->class_w.assign(groups, 0);
-  for (unsigned g = 0; g < groups; ++g) {
-    unsigned w = ~0u;
-    for (unsigned j = 0; j < G; ++j) {
-      const int sm = whole[g * G + j];
-      ctx->h_slot[sm] = g * G + j;
-      w = std::min(w, class_weight(c, c.cls[sm]));
-    }
-    ctx->class_w[g] = w;
-  }
+// One sweep CTA on every SM (the grid covers the SMs and two CTAs cannot share
+// one): CTA slots are pinned to SMs (slot = %smid), so a row group is the same
+// physical SMs in every launch and a static weighted row split
+// (UOT_SCHEDULE_WEIGHTED) stays attached to the SMs it was measured on.
+void plan_pinning(uot_ctx* ctx, int smem_optin) {
+  ctx->pinned = ctx->grid == static_cast<unsigned>(ctx->sms) &&
+                2 * ctx->smem > static_cast<size_t>(smem_optin) + 1024;
+}
+
+// Row bounds of the groups from integer weights: group g owns
+// [rows * W(g) / W, rows * W(g+1) / W) with W(g) the prefix sum.
+std::vector<unsigned long long> weighted_bounds(uint64_t rows, const std::vector<uint32_t>& w) {
   uint64_t wsum = 0;
-  for (unsigned w : ctx->class_w) wsum += w;
-  ctx->h_gbounds.assign(groups + 1, 0);
+  for (uint32_t x : w) wsum += x;
+  std::vector<unsigned long long> b(w.size() + 1, 0);
   uint64_t acc = 0;
-  for (unsigned g = 0; g < groups; ++g) {
-    acc += ctx->class_w[g];
-    // rows * acc / wsum without overflow for any realistic row count
-    const unsigned __int128 b = static_cast<unsigned __int128>(ctx->rows) * acc / wsum;
-    ctx->h_gbounds[g + 1] = static_cast<unsigned long long>(b);
+  for (size_t g = 0; g < w.size(); ++g) {
+    acc += w[g];
+    b[g + 1] = static_cast<unsigned long long>(static_cast<unsigned __int128>(rows) * acc / wsum);
   }
-  ctx->class_ok = true;
-  ctx->nclasses = static_cast<int>(c.class_ms.size());
+  return b;
 }
 
 int plan_layout(uot_ctx* ctx) {
@@ -543,7 +396,7 @@ int plan_layout(uot_ctx* ctx) {
   ctx->full = slice == epc * cfg->nt * cfg->v ? 1 : 0;
   int rc = probe_smid_map(ctx);
   if (rc) return rc;
-  plan_class_schedule(ctx, smem_optin);
+  plan_pinning(ctx, smem_optin);
   for (SweepFn fn : {cfg->iter[ctx->full], cfg->seed[ctx->full]}) {
     if (!fn) continue;
     const int rc = ctx->cuda(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
@@ -600,13 +453,12 @@ int alloc_all(uot_ctx* ctx) {
   if ((rc = dalloc(ctx, &ctx->mail, mn))) return rc;
   if ((rc = dalloc(ctx, &ctx->d_dbg, 2 * static_cast<size_t>(ctx->grid)))) return rc;
   CK(cudaMemsetAsync(ctx->d_dbg, 0, 2 * sizeof(unsigned) * ctx->grid, ctx->stream));
-  if (ctx->class_ok) {
-    if ((rc = dalloc(ctx, &ctx->d_slot, ctx->h_slot.size()))) return rc;
-    if ((rc = dalloc(ctx, &ctx->d_gbounds, ctx->h_gbounds.size()))) return rc;
-    CK(cudaMemcpyAsync(ctx->d_slot, ctx->h_slot.data(), sizeof(unsigned) * ctx->h_slot.size(), cudaMemcpyHostToDevice,
-                       ctx->stream));
-    CK(cudaMemcpyAsync(ctx->d_gbounds, ctx->h_gbounds.data(), sizeof(unsigned long long) * ctx->h_gbounds.size(),
-                       cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->pinned) {
+    std::vector<unsigned> slot(ctx->sms);
+    for (int i = 0; i < ctx->sms; ++i) slot[i] = static_cast<unsigned>(i);
+    if ((rc = dalloc(ctx, &ctx->d_slot, slot.size()))) return rc;
+    if ((rc = dalloc(ctx, &ctx->d_gbounds, static_cast<size_t>(ctx->groups) + 1))) return rc;
+    CK(cudaMemcpy(ctx->d_slot, slot.data(), sizeof(unsigned) * slot.size(), cudaMemcpyHostToDevice));
   }
   CK(cudaMemsetAsync(ctx->mail, 0, mn * sizeof(ulonglong2), ctx->stream));
   if ((rc = dalloc(ctx, &ctx->ctl, 1))) return rc;
@@ -656,11 +508,8 @@ SweepArgs sweep_args(const uot_ctx* ctx) {
   a.evict_first = ctx->evict_first;
   a.smid_map = ctx->smid_map;
   a.dyn = ctx->dyn;
-  // class-grouped slots for the class-weighted and the dynamic schedule; the
-  // weighted row blocks for the former only (uniform: balanced_blocks, smid_map)
-  const bool cls = ctx->class_ok && ctx->schedule != UOT_SCHEDULE_UNIFORM;
-  a.slot_of_sm = cls ? ctx->d_slot : nullptr;
-  a.gbounds = cls && ctx->schedule == UOT_SCHEDULE_CLASS_WEIGHTED ? ctx->d_gbounds : nullptr;
+  a.slot_of_sm = ctx->pinned ? ctx->d_slot : nullptr;
+  a.gbounds = ctx->pinned && ctx->schedule == UOT_SCHEDULE_WEIGHTED ? ctx->d_gbounds : nullptr;
   a.dbg = ctx->d_dbg;
   a.mail = ctx->mail;
   a.fi = ctx->fi;
@@ -695,7 +544,7 @@ int launch_sweep(uot_ctx* ctx, bool seed) {
   // smid_map a CTA's identity is its SM — only a co-resident grid (one CTA per
   // SM) makes that a permutation, even for the seed sweep, when other kernels
   // share the GPU (e.g. the ranks of a session group on one device)
-  const bool xchg = ctx->G > 1 || (ctx->class_ok && ctx->schedule != UOT_SCHEDULE_UNIFORM);
+  const bool xchg = ctx->G > 1 || ctx->pinned;
   SweepFn fn = seed ? ctx->cfg->seed[ctx->full] : ctx->cfg->iter[ctx->full];
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctx->grid);
@@ -1088,15 +937,41 @@ int uot_exchange_mode(const uot_ctx* ctx) { return ctx ? ctx->xmode : -1; }
 
 int uot_set_schedule(uot_ctx* ctx, int schedule) {
   if (!ctx) return UOT_INVALID_PARAMETER;
-  if (schedule != UOT_SCHEDULE_CLASS_WEIGHTED && schedule != UOT_SCHEDULE_UNIFORM && schedule != UOT_SCHEDULE_DYNAMIC)
+  if (schedule != UOT_SCHEDULE_UNIFORM && schedule != UOT_SCHEDULE_WEIGHTED && schedule != UOT_SCHEDULE_DYNAMIC)
     return ctx->fail(UOT_INVALID_PARAMETER, "unknown row-batch schedule %d", schedule);
+  if (schedule == UOT_SCHEDULE_WEIGHTED && (!ctx->pinned || ctx->weights.size() != ctx->groups))
+    return ctx->fail(UOT_CONFIG_ERROR, "the weighted schedule needs one sweep CTA per SM and group weights "
+                                       "(uot_set_group_weights / uot_calibrate_schedule)");
   ctx->schedule = schedule;
   ctx->dyn = schedule == UOT_SCHEDULE_DYNAMIC && !ctx->wide ? 1 : 0;
   return UOT_OK;
 }
 
 int uot_set_deterministic(uot_ctx* ctx, int on) {
-  return uot_set_schedule(ctx, on ? UOT_SCHEDULE_CLASS_WEIGHTED : UOT_SCHEDULE_DYNAMIC);
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  if (on) return uot_set_schedule(ctx, ctx->weights.size() == ctx->groups && ctx->pinned ? UOT_SCHEDULE_WEIGHTED
+                                                                                        : UOT_SCHEDULE_UNIFORM);
+  return uot_set_schedule(ctx, UOT_SCHEDULE_DYNAMIC);
+}
+
+int uot_set_group_weights(uot_ctx* ctx, const uint32_t* w, uint32_t n) {
+  if (!ctx || !w) return UOT_INVALID_PARAMETER;
+  if (!ctx->pinned)
+    return ctx->fail(UOT_CONFIG_ERROR, "weighted row blocks need one sweep CTA on every SM (grid %u, %d SMs)",
+                     ctx->grid, ctx->sms);
+  if (n != ctx->groups) return ctx->fail(UOT_INVALID_PARAMETER, "%u weights for %u row groups", n, ctx->groups);
+  uint64_t sum = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (w[i] < 1 || w[i] > (1u << 20)) return ctx->fail(UOT_INVALID_PARAMETER, "group weight %u out of [1, 2^20]", w[i]);
+    sum += w[i];
+  }
+  ctx->weights.assign(w, w + n);
+  const auto b = weighted_bounds(ctx->rows, ctx->weights);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(ctx->d_gbounds, b.data(), sizeof(unsigned long long) * b.size(), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return uot_set_schedule(ctx, UOT_SCHEDULE_WEIGHTED);
 }
 
 int uot_get_schedule_stats(const uot_ctx* cctx, uint32_t* cta_smid, uint32_t* cta_batches, uint32_t* group_weight) {
@@ -1111,24 +986,87 @@ int uot_get_schedule_stats(const uot_ctx* cctx, uint32_t* cta_smid, uint32_t* ct
     if (cta_batches) cta_batches[c] = h[2 * c + 1];
   }
   if (group_weight)
-    for (unsigned g = 0; g < ctx->groups; ++g) group_weight[g] = ctx->class_ok ? ctx->class_w[g] : 32u;
+    for (unsigned g = 0; g < ctx->groups; ++g)
+      group_weight[g] = ctx->weights.size() == ctx->groups ? ctx->weights[g] : 1u;
   return UOT_OK;
 }
 
-int uot_get_sm_classes(int device, int32_t* cls, double* probe_ms, int n) {
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+// Calibration of the weighted schedule: `k` dynamic iterations on a scratch
+// copy of the plan (the session's plan, factors, column sums and stop state are
+// untouched; only never-reset exchange tags advance), the row batches each
+// group took become its weight. Deterministic afterwards: the weights are
+// fixed, so every later solve with them is bit-reproducible.
+int uot_calibrate_schedule(uot_ctx* ctx, uint32_t k) {
+  if (!ctx) return UOT_INVALID_PARAMETER;
+  if (!ctx->have_problem || !ctx->seeded)
+    return ctx->fail(UOT_INVALID_PARAMETER, "calibration needs a problem and its column sums (init_col_sums)");
+  if (!ctx->pinned)
+    return ctx->fail(UOT_CONFIG_ERROR, "weighted row blocks need one sweep CTA on every SM (grid %u, %d SMs)",
+                     ctx->grid, ctx->sms);
+  if (ctx->variant != UOT_VARIANT_FUSED || ctx->wide)
+    return ctx->fail(UOT_CONFIG_ERROR, "calibration runs the fused sweep");
+  k = std::max<uint32_t>(2, std::min<uint32_t>(k, 64));
+  CK(cudaSetDevice(ctx->device));
+  const size_t pbytes = static_cast<size_t>(ctx->rows) * ctx->pitch * ctx->esz;
+  void* scratch = nullptr;
+  if (cudaMalloc(&scratch, pbytes) != cudaSuccess) {
     cudaGetLastError();
-    return UOT_INVALID_PARAMETER;
+    return ctx->fail(UOT_CONFIG_ERROR, "not enough device memory for a calibration copy of the plan (%zu bytes)",
+                     pbytes);
   }
-  if (cudaSetDevice(device) != cudaSuccess) return UOT_CUDA_ERROR;
-  const SmClasses& c = sm_classes(device);
-  if (c.ms.empty()) return UOT_CUDA_ERROR;
-  for (int i = 0; i < n && i < static_cast<int>(c.ms.size()); ++i) {
-    if (cls) cls[i] = c.ok ? c.cls[i] : -1;
-    if (probe_ms) probe_ms[i] = c.ms[i];
+  // saved state: factors, column sums, control
+  std::vector<double> sb(2 * static_cast<size_t>(ctx->pitch)), sc(ctx->cols), sa(ctx->rows);
+  Control* saved = nullptr;
+  int rc = ctx->cuda(cudaMalloc(reinterpret_cast<void**>(&saved), sizeof(Control)), "cudaMalloc");
+  if (!rc) rc = ctx->cuda(cudaMemcpyAsync(scratch, ctx->P, pbytes, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+  if (!rc) rc = ctx->cuda(cudaMemcpyAsync(saved, ctx->ctl, sizeof(Control), cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+  if (!rc) rc = ctx->cuda(cudaMemcpyAsync(sb.data(), ctx->beta2, sb.size() * 8, cudaMemcpyDeviceToHost, ctx->stream), "copy");
+  if (!rc) rc = ctx->cuda(cudaMemcpyAsync(sc.data(), ctx->col_sums, sc.size() * 8, cudaMemcpyDeviceToHost, ctx->stream), "copy");
+  if (!rc) rc = ctx->cuda(cudaMemcpyAsync(sa.data(), ctx->alpha, sa.size() * 8, cudaMemcpyDeviceToHost, ctx->stream), "copy");
+  void* real = ctx->P;
+  const int sched = ctx->schedule, dyn = ctx->dyn;
+  std::vector<uint64_t> counts(ctx->groups, 0);
+  if (!rc) {
+    ctx->P = scratch;
+    ctx->schedule = UOT_SCHEDULE_DYNAMIC;
+    ctx->dyn = 1;
+    begin_iterate_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctl, 1e-300);
+    std::vector<unsigned> h(2 * static_cast<size_t>(ctx->grid));
+    for (uint32_t i = 0; i < k && !rc; ++i) {
+      rc = launch_sweep(ctx, false);
+      if (!rc) rc = launch_finalize_single<kFinIter>(ctx);  // local finalize: no peer exchange for a scratch run
+      if (!rc) rc = ctx->cuda(cudaMemcpyAsync(h.data(), ctx->d_dbg, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream), "copy");
+      if (!rc) rc = ctx->cuda(cudaStreamSynchronize(ctx->stream), "calibration sweep");
+      if (i == 0) continue;  // warm-up
+      for (unsigned g = 0; g < ctx->groups && !rc; ++g) counts[g] += h[2 * (g * ctx->G) + 1];
+    }
+    ctx->P = real;
+    ctx->schedule = sched;
+    ctx->dyn = dyn;
   }
-  return c.ok ? UOT_OK : UOT_CONFIG_ERROR;
+  if (!rc) rc = ctx->cuda(cudaMemcpyAsync(ctx->beta2, sb.data(), sb.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy");
+  if (!rc) rc = ctx->cuda(cudaMemcpyAsync(ctx->col_sums, sc.data(), sc.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy");
+  if (!rc) rc = ctx->cuda(cudaMemcpyAsync(ctx->alpha, sa.data(), sa.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy");
+  if (!rc) {
+    restore_control_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctl, saved);
+    ctx->launches++;
+    rc = ctx->cuda(cudaStreamSynchronize(ctx->stream), "calibration restore");
+  }
+  cudaFree(scratch);
+  if (saved) cudaFree(saved);
+  if (rc) return rc;
+  if ((rc = sync_ctl(ctx))) return rc;
+  std::vector<uint32_t> w(ctx->groups);
+  for (unsigned g = 0; g < ctx->groups; ++g)
+    w[g] = static_cast<uint32_t>(std::min<uint64_t>(1u << 20, std::max<uint64_t>(1, counts[g])));
+  return uot_set_group_weights(ctx, w.data(), ctx->groups);
+}
+
+int uot_get_group_weights(const uot_ctx* ctx, uint32_t* w, uint32_t n) {
+  if (!ctx || !w) return UOT_INVALID_PARAMETER;
+  if (ctx->weights.size() != ctx->groups || n < ctx->groups) return UOT_INVALID_PARAMETER;
+  std::copy(ctx->weights.begin(), ctx->weights.end(), w);
+  return UOT_OK;
 }
 
 int uot_set_resident(uot_ctx* ctx, int on) {
@@ -1206,7 +1144,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->dtype = ctx->dtype;
   o->dynamic = ctx->dyn;
   o->schedule = ctx->schedule;
-  o->sm_classes = ctx->class_ok ? ctx->nclasses : 0;
+  o->pinned = ctx->pinned ? 1 : 0;
   o->nbuf = ctx->cfg->nbuf;
   o->sms = ctx->sms;
   o->rank = ctx->rank;

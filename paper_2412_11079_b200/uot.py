@@ -90,7 +90,7 @@ class Layout(C.Structure):
                 ("nranks", C.c_int32), ("device", C.c_int32), ("evict_first", C.c_int32),
                 ("smid_map", C.c_int32), ("exchange", C.c_int32),
                 ("resident", C.c_int32), ("dtype", C.c_int32),
-                ("dynamic", C.c_int32), ("schedule", C.c_int32), ("sm_classes", C.c_int32),
+                ("dynamic", C.c_int32), ("schedule", C.c_int32), ("pinned", C.c_int32),
                 ("variant", C.c_int32)]
 
     def as_dict(self):
@@ -132,7 +132,9 @@ def lib():
     L.uot_set_resident.argtypes = [_P, _i]
     L.uot_set_schedule.argtypes = [_P, _i]
     L.uot_get_schedule_stats.argtypes = [_P, _P, _P, _P]
-    L.uot_get_sm_classes.argtypes = [_i, _P, _P, _i]
+    L.uot_set_group_weights.argtypes = [_P, _P, C.c_uint32]
+    L.uot_get_group_weights.argtypes = [_P, _P, C.c_uint32]
+    L.uot_calibrate_schedule.argtypes = [_P, C.c_uint32]
     L.uot_problem_file_info.argtypes = [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_i),
                                         C.POINTER(_d), C.POINTER(_d)]
     L.uot_last_io_error.restype = C.c_char_p
@@ -586,20 +588,38 @@ class Session:
             _raise(1, f"unknown iteration variant {name!r}")
         self._check(lib().uot_set_variant(self._h, self.VARIANTS[name]))
 
-    SCHEDULES = {"class_weighted": 0, "uniform": 1, "dynamic": 2}
+    SCHEDULES = {"uniform": 0, "weighted": 1, "dynamic": 2}
 
     def set_schedule(self, name: str):
-        """Row-batch schedule of the sweep (uot_set_schedule): "class_weighted"
-        (default; static row blocks sized by the SMs' HBM speed class,
-        bit-reproducible), "uniform" (balanced_blocks) or "dynamic"."""
+        """Row-batch schedule of the sweep (uot_set_schedule): "uniform"
+        (default; balanced_blocks, bit-reproducible), "weighted" (static blocks
+        from group weights, bit-reproducible for given weights) or "dynamic"."""
         if name not in self.SCHEDULES:
             _raise(1, f"unknown schedule {name!r}")
         self._check(lib().uot_set_schedule(self._h, self.SCHEDULES[name]))
         self._refresh_layout()
 
+    def set_group_weights(self, w):
+        """Per-row-group weights (uot_set_group_weights); selects "weighted"."""
+        w = np.ascontiguousarray(w, np.uint32)
+        self._check(lib().uot_set_group_weights(self._h, _ptr(w), w.size))
+        self._refresh_layout()
+
+    def group_weights(self) -> np.ndarray:
+        w = np.zeros(self.layout["groups"], np.uint32)
+        self._check(lib().uot_get_group_weights(self._h, _ptr(w), w.size))
+        return w
+
+    def calibrate_schedule(self, k: int = 4) -> np.ndarray:
+        """Measure per-group weights with k dynamic iterations on a scratch copy
+        of the plan (uot_calibrate_schedule); selects "weighted"."""
+        self._check(lib().uot_calibrate_schedule(self._h, int(k)))
+        self._refresh_layout()
+        return self.group_weights()
+
     def set_deterministic(self, on: bool = True):
-        """on: the class-weighted static schedule (default, bit-reproducible run
-        to run); off: the dynamic batch counter (uot_set_deterministic)."""
+        """on: a static schedule (weighted when weights are set, else uniform;
+        bit-reproducible run to run); off: the dynamic batch counter."""
         self._check(lib().uot_set_deterministic(self._h, 1 if on else 0))
         self._refresh_layout()
 
@@ -807,15 +827,3 @@ def _cached_session(m: int, n: int, device: int, dtype=np.float32) -> "Session":
         _tls.session, _tls.key = Session(m, n, device, dtype=dtype), key
     return _tls.session
 
-
-def sm_classes(device: int = 0):
-    """(class per SM, probe ms per SM) of `device` (topology.cuh); class -1
-    everywhere when the probe found no crisp speed classes."""
-    n = 1024
-    cls = np.full(n, -1, np.int32)
-    ms = np.zeros(n, np.float64)
-    rc = lib().uot_get_sm_classes(int(device), _ptr(cls), _ptr(ms), n)
-    if rc not in (0, 4):
-        _raise(rc, "uot_get_sm_classes failed")
-    k = int(np.count_nonzero(ms))
-    return cls[:k], ms[:k]

@@ -89,73 +89,77 @@ def test_resident_degenerate_column_sums_raise(gpu, orc):
 @pytest.mark.parametrize("m,n,k", [(3000, 32768, 4), (20000, 4096, 5), (4099, 8192, 4)])
 def test_batch_schedules(gpu, orc, m, n, k):
     """The three row-batch schedules (uot_set_schedule) meet the parity bar; the
-    two static ones reproduce themselves bit for bit."""
+    two static ones reproduce themselves bit for bit (weighted: for the same
+    weights, in another session)."""
     a, rpd, cpd = orc.gen_problem(11, m, n)
     ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 4)
     out = {}
-    for name, mode in (("cw1", "class_weighted"), ("cw2", "class_weighted"), ("u1", "uniform"),
-                       ("u2", "uniform"), ("dyn", "dynamic")):
+    weights = None
+    for name in ("u1", "u2", "w1", "w2", "dyn"):
         with gpu.Session(m, n) as s:
-            s.set_schedule(mode)
-            assert s.layout["schedule"] == gpu.Session.SCHEDULES[mode]
-            assert s.layout["dynamic"] == (1 if mode == "dynamic" else 0)
             s.set_problem(gpu.Problem(a, rpd, cpd, 1.0, 0.1))
             s.init_col_sums()
+            if name == "w1":
+                weights = s.calibrate_schedule(3)  # the plan is untouched by the scratch run
+                assert np.array_equal(s.plan(), a)
+            elif name == "w2":
+                s.set_group_weights(weights)
+            elif name == "dyn":
+                s.set_schedule("dynamic")
+            mode = {"u": "uniform", "w": "weighted", "d": "dynamic"}[name[0]]
+            assert s.layout["schedule"] == gpu.Session.SCHEDULES[mode]
+            assert s.layout["dynamic"] == (1 if mode == "dynamic" else 0)
             it, err, conv = s.iterate(k, KNEVER)
             assert it == k
             out[name] = (s.plan(), s.factors(), s.col_sums())
         assert_parity(out[name][0], ref.plan, rpd, cpd, f"{m}x{n} {name}")
         np.testing.assert_allclose(out[name][1].alpha, ref.alpha, rtol=1e-10)
-    for x, y in (("cw1", "cw2"), ("u1", "u2")):
+    for x, y in (("u1", "u2"), ("w1", "w2")):
         assert np.array_equal(out[x][0], out[y][0])
         np.testing.assert_array_equal(out[x][1].alpha, out[y][1].alpha)
         np.testing.assert_array_equal(out[x][2], out[y][2])
 
 
 @pytest.mark.slow
-def test_default_schedule_is_bit_reproducible_at_scale(gpu, orc):
-    """Two default runs (separate sessions) of a problem far past the 64 MiB
+def test_default_schedule_is_bit_reproducible_at_scale(gpu):
+    """Two default runs (separate sessions) of problems far past the 64 MiB
     threshold give identical bits: plan, factors, carried column sums and error
-    (the reference's promise, fused.hpp:193-196, 242-248)."""
-    m, n, k = 16384, 20000, 6  # 1.2 GiB, G = 3 ... and one CTA per SM where the grid allows
-    runs = []
-    for _ in range(2):
-        with gpu.Session(m, n) as s:
-            assert s.layout["schedule"] == 0 and s.layout["dynamic"] == 0
-            s.generate_problem(42, 1.0, 0.1)
-            s.init_col_sums()
-            it, err, conv = s.iterate(k, KNEVER)
-            f = s.factors()
-            runs.append((s.plan(), f.alpha, f.beta, s.col_sums(), err))
-    for x, y in zip(runs[0], runs[1]):
-        assert np.array_equal(np.asarray(x), np.asarray(y))
-    for (m, n) in [(8192, 32768), (65536, 4096)]:  # G = 4 and G = 1 with one CTA per SM
+    (the reference's promise, fused.hpp:193-196, 242-248); G = 3, 4 and 1."""
+    for (m, n, k) in [(16384, 20000, 6), (8192, 32768, 5), (65536, 4096, 5)]:
         runs = []
         for _ in range(2):
             with gpu.Session(m, n) as s:
-                s.generate_problem(7, 1.0, 0.1)
+                assert s.layout["schedule"] == 0 and s.layout["dynamic"] == 0
+                s.generate_problem(42, 1.0, 0.1)
                 s.init_col_sums()
-                s.iterate(4, KNEVER)
-                runs.append((s.plan(), s.factors().beta, s.layout["sm_classes"]))
-        assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
-        assert runs[0][2] == runs[1][2]
+                it, err, conv = s.iterate(k, KNEVER)
+                f = s.factors()
+                runs.append((s.plan(), f.alpha, f.beta, s.col_sums(), err))
+        for x, y in zip(runs[0], runs[1]):
+            assert np.array_equal(np.asarray(x), np.asarray(y)), f"{m}x{n}"
 
 
-def test_sm_classes_and_weighted_blocks(gpu):
-    """The probe's classes drive the schedule: every CTA's SM is recorded, the
-    groups' weights are per class, and a class-weighted sweep streams every row
-    exactly once (batch counts add up to the rows)."""
-    cls, ms = gpu.sm_classes(0)
-    assert cls.size == ms.size and cls.size >= 1
+def test_calibration_leaves_the_session_state(gpu, orc):
+    """uot_calibrate_schedule runs on a scratch copy: plan, factors, column sums
+    and the iteration count are unchanged, and the weighted solve continues
+    exactly where the session was (== the uniform solve to the parity bar)."""
     m, n = 20000, 4096
+    a, rpd, cpd = orc.gen_problem(3, m, n)
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, 5, 4)
     with gpu.Session(m, n) as s:
-        s.generate_problem(3, 1.0, 0.1)
+        s.set_problem(gpu.Problem(a, rpd, cpd, 1.0, 0.1))
         s.init_col_sums()
         s.iterate(2, KNEVER)
-        smid, nb, w = s.schedule_stats()
-        lay = s.layout
-    assert len(set(smid.tolist())) == smid.size  # one CTA per SM
-    rows_per_batch = lay["rows_per_step"]
-    assert nb.sum() * rows_per_batch >= m and (nb.sum() - smid.size) * rows_per_batch < m
-    if lay["sm_classes"] > 0:
-        assert len(set(w.tolist())) <= lay["sm_classes"] + 1
+        before = (s.plan(), s.factors(), s.col_sums(), s.report())
+        w = s.calibrate_schedule(4)
+        after = (s.plan(), s.factors(), s.col_sums(), s.report())
+        assert w.size == s.layout["groups"] and w.min() >= 1 and s.layout["pinned"] == 1
+        assert np.array_equal(before[0], after[0]) and np.array_equal(before[2], after[2])
+        np.testing.assert_array_equal(before[1].alpha, after[1].alpha)
+        np.testing.assert_array_equal(before[1].beta, after[1].beta)
+        assert before[3] == after[3]
+        it, err, conv = s.iterate(3, KNEVER)
+        assert it == 3
+        smid, nb, gw = s.schedule_stats()
+        assert len(set(smid.tolist())) == smid.size and np.array_equal(gw, w)
+        assert_parity(s.plan(), ref.plan, rpd, cpd, "weighted after calibration")
