@@ -143,7 +143,10 @@ void test_errors_map_to_reference_exceptions() {
 
 void test_single_rank_distributed() {  // test_distributed.cpp:92-104, 142-155
   const auto p = random_problem(24, 64, 64, 0.5);
+  // a real id: with one rank and an id the session runs the NCCL exchange path
+  // (a one-rank communicator, ncclAllReduce per iteration)
   std::uint8_t id[128] = {0};
+  CHECK(uot_nccl_unique_id(id) == UOT_OK);
   const auto d = uot::cuda::distributed_solve(p, kNever, 37, 0, 1, id, 0);
   const auto ref = uot::distributed_solve(p, kNever, 37, std::size_t(1));
   CHECK(d.report.iterations == 37 && d.report.solver == "dist");

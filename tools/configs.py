@@ -2,7 +2,10 @@
 device-timed iterations/s and model HBM GB/s (2*R*C*4 bytes per iteration,
 metrics.cpp:69-72) next to the measured copy peak (MEASURED_PEAKS.json).
 
-python tools/configs.py [--json OUT] [--only 2,4]
+python tools/configs.py [--json OUT] [--only 2,4] [--schedule uniform|weighted|dynamic]
+
+--schedule: the row-batch schedule (default: the session default, uniform
+static blocks; weighted calibrates its weights once, untimed).
 """
 import json
 import os
@@ -32,11 +35,18 @@ for idx, (name, m, n, k) in enumerate(CONFIGS, 1):
     with uot.Session(m, n) as s:
         s.generate_problem(42, 1.0, 0.1)
         s.init_col_sums()
+        sched = sys.argv[sys.argv.index("--schedule") + 1] if "--schedule" in sys.argv else None
+        if sched == "weighted" and not s.layout["pinned"]:
+            sched = "uniform"
+        if sched == "weighted":
+            s.calibrate_schedule(4)
+        if sched:
+            s.set_schedule(sched)
         s.iterate(3, 1e-300)  # warm-up
         it, err, conv, ms = s.iterate_timed(k, 1e-300)
         lay = s.layout
     gbs = 2 * m * n * 4 * it / (ms * 1e-3) / 1e9
-    mode = "resident" if lay["resident"] else f"streaming G={lay['G']}"
+    mode = "resident" if lay["resident"] else f"streaming G={lay['G']} {sched or 'default'}"
     rows.append({"config": name, "iterations": it, "ms_total": ms, "us_per_iter": ms * 1e3 / it,
                  "it_per_s": it / (ms * 1e-3), "model_gbs": gbs, "frac_of_copy_peak": gbs / peak, "mode": mode})
     print(f"{name:34s} {ms * 1e3 / it:9.1f} us/iter {it / (ms * 1e-3):10.1f} it/s {gbs:7.0f} GB/s "
