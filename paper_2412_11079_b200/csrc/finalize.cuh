@@ -95,7 +95,10 @@ __device__ __forceinline__ double* peer_recv(unsigned char* base, unsigned nrank
   return reinterpret_cast<double*>(base + PeerRegion::flag_bytes(nranks));
 }
 
-template <int MODE, bool REDUCE, bool BETA, int XCH = kXchNone>
+// R > 0: every thread issues its R partial-row loads at once (groups <= 8R);
+// R = 0: batches of 8 (any number of groups). R sets the register footprint, so
+// the launch picks the smallest that covers the groups (one wave of blocks).
+template <int MODE, bool REDUCE, bool BETA, int XCH = kXchNone, int R = 0>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArgs f) {
   __shared__ double part[kFinSlices][kFinCols];
   __shared__ double red[kFinSlices];
@@ -108,22 +111,46 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
   const unsigned long long seq = ctl->xseq + 1;  // this exchange (kXchPeer)
   const unsigned par = static_cast<unsigned>(seq & 1ull);
 
+  // The alpha error of a single-rank iteration: block 0 reduces the sweep CTAs'
+  // slots while the column loads of every block are in flight, and hands the
+  // max to the last block through the control block (published before block
+  // 0's election increment), so the last block's tail is only the stop test.
+  if (REDUCE && BETA && MODE == kFinIter && blockIdx.x == 0) {
+    const double ea = block_alpha_err(f, red);
+    if (threadIdx.x == 0) ctl->fin_alpha_err = ea;
+  }
+
   double s = 0.0;  // column sum of column j (valid in warp 0)
   if (REDUCE) {
-    // Same ascending-k order of additions as a plain loop, with the L2 loads of
-    // 8 rows issued together (a serial loop paid one L2 round trip per row:
-    // 13 us at 148 groups).
+    // Same ascending-k order of additions as a plain loop, with every L2 load
+    // of the thread's rows (k = slice, slice + 8, ...) issued before the first
+    // add: one round trip instead of one per batch of rows (a serial loop paid
+    // one per row: 13 us at 148 groups).
     double p = 0.0;
     if (j < f.cols) {
-      unsigned k = slice;
-      for (; k + 7 * kFinSlices < f.groups; k += 8 * kFinSlices) {
-        double v[8];
+      if (R > 0) {
+        double v[R > 0 ? R : 1];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(&f.partials[static_cast<size_t>(k + u * kFinSlices) * f.pitch + j]);
+        for (int u = 0; u < R; ++u) {
+          const unsigned k = slice + u * kFinSlices;
+          v[u] = k < f.groups ? __ldcg(&f.partials[static_cast<size_t>(k) * f.pitch + j]) : 0.0;
+        }
+        p = v[0];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) p += v[u];
+        for (int u = 1; u < R; ++u)
+          if (slice + u * kFinSlices < f.groups) p += v[u];
+      } else {
+        unsigned k = slice;
+        for (; k + 7 * kFinSlices < f.groups; k += 8 * kFinSlices) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            v[u] = __ldcg(&f.partials[static_cast<size_t>(k + u * kFinSlices) * f.pitch + j]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) p += v[u];
+        }
+        for (; k < f.groups; k += kFinSlices) p += __ldcg(&f.partials[static_cast<size_t>(k) * f.pitch + j]);
       }
-      for (; k < f.groups; k += kFinSlices) p += __ldcg(&f.partials[static_cast<size_t>(k) * f.pitch + j]);
     }
     part[slice][lane] = p;
     __syncthreads();
@@ -226,7 +253,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinalizeArg
   double ea = 0.0;
   if (MODE == kFinIter) {
     if (REDUCE) {
-      ea = block_alpha_err(f, red);
+      ea = *reinterpret_cast<volatile double*>(&ctl->fin_alpha_err);  // block 0's reduction
     } else if (XCH == kXchPeer) {
       const double* recv = peer_recv(f.region, f.nranks) + static_cast<size_t>(par) * f.nranks * f.xlen;
       for (unsigned q = 0; q < f.nranks; ++q) {

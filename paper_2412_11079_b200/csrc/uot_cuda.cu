@@ -656,7 +656,15 @@ template <int MODE>
 int launch_finalize_single(uot_ctx* ctx) {
   const unsigned blocks = finalize_blocks(ctx->pitch);
   ctx->launches++;
-  finalize_kernel<MODE, true, true><<<blocks, kFinThreads, 0, ctx->stream>>>(fin_args(ctx));
+  // all of a thread's partial-row loads in flight at once (one L2 round trip),
+  // with the smallest register footprint that covers the groups
+  const FinalizeArgs f = fin_args(ctx);
+  if (ctx->groups <= 5 * kFinSlices)
+    finalize_kernel<MODE, true, true, kXchNone, 5><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
+  else if (ctx->groups <= 20 * kFinSlices)
+    finalize_kernel<MODE, true, true, kXchNone, 20><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
+  else
+    finalize_kernel<MODE, true, true><<<blocks, kFinThreads, 0, ctx->stream>>>(f);
   return ctx->cuda(cudaGetLastError(), "finalize launch");
 }
 

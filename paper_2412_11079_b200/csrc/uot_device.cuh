@@ -41,6 +41,7 @@ struct Control {
   double rerr_alpha[3];       // resident kernel: max|alpha(t)-1| at slot t%3
   unsigned long long batch_next;  // dynamic sweep: next batch to hand out (0 between sweeps)
   unsigned long long sweep_seq;   // never reset: completed sweep + finalize pairs (mail tags)
+  double fin_alpha_err;           // single-rank finalize: block 0's max|alpha-1| for the last block
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

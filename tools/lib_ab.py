@@ -37,9 +37,11 @@ def inner():
                     sched = "uniform"
             s.set_schedule(sched)
             s.iterate(5, 1e-300)
-            s.set_timing(True)
-            it, _, _, ms = s.iterate_timed(k, 1e-300)
+            it, _, _, ms = s.iterate_timed(k, 1e-300)  # whole-step time, no per-kernel events
+            s.set_timing(True)  # per-kernel breakdown on a separate short run (events add gaps)
+            s.iterate(min(k, 50), 1e-300)
             sw, fin, ns = s.timing()
+            s.set_timing(False)
             row = {"shape": spec, "schedule": sched, "us_iter": ms / it * 1e3, "sweep_us": sw / ns * 1e3,
                    "fin_us": fin / ns * 1e3, "gbs": 2 * m * n * 4 / (ms / it * 1e-3) / 1e9}
             sus = float(arg("--sustained-s", 0))
@@ -47,7 +49,6 @@ def inner():
                 import statistics
                 import subprocess
                 import time
-                s.set_timing(False)
                 ks = max(k, int(sus / (ms / it * 1e-3)))
                 smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits",
                                         "-lms", "100"], stdout=subprocess.PIPE, text=True)
