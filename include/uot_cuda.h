@@ -184,9 +184,11 @@ UOT_API int uot_set_deterministic(uot_ctx* ctx, int on);
  * slots g*G .. g*G+G-1 = SMs g*G .. ; selects WEIGHTED. */
 UOT_API int uot_set_group_weights(uot_ctx* ctx, const uint32_t* weights, uint32_t n);
 UOT_API int uot_get_group_weights(const uot_ctx* ctx, uint32_t* weights, uint32_t n);
-/* Measure the weights: k dynamic iterations (k in [2, 64], the first
- * discarded) of the fused sweep on a scratch copy of the plan; each group's
- * weight is the row batches it took. The session's plan, factors, column sums
+/* Measure the weights on a scratch copy of the plan: k dynamic iterations
+ * (k in [2, 64], the first discarded) give each group's first weight (the row
+ * batches it took), then three rounds of two weighted iterations rescale each
+ * weight by (mean completion time / the group's completion time)^0.75, so the
+ * static row blocks finish together. The session's plan, factors, column sums
  * and stop state are unchanged. Needs a problem and init_col_sums; selects
  * WEIGHTED. Store the weights (uot_get_group_weights) to reuse them across
  * sessions and processes on the same GPU. */

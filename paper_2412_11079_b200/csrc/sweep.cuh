@@ -63,7 +63,7 @@ struct SweepArgs {
   int smid_map;               // CTA slot = %smid (the grid covers every SM exactly once)
   const unsigned* slot_of_sm; // [#SMs] CTA slot of each SM (class-grouped row groups), or nullptr
   const unsigned long long* gbounds;  // [groups+1] static row block of each group, or nullptr (balanced)
-  unsigned* dbg;              // [grid][2] {smid, batches} of the last sweep (schedule statistics)
+  unsigned* dbg;              // [grid][kDbg] {smid, batches, start, end ns} of the last sweep (schedule statistics)
   int dyn;                    // batches handed out by a global counter (else a static row block)
   ulonglong2* mail;           // [groups][kMail] {first row, tag}: the group leader's batch picks (dyn, G > 1)
   double fi;
@@ -96,6 +96,7 @@ __host__ __device__ constexpr int tr_slot(int id) {
 #endif
 
 constexpr int kRing = 8;   // exchange records per CTA
+constexpr int kDbg = 4;    // schedule statistics per CTA: SM id, row batches, producer start / end (globaltimer ns, low 32 bits)
 constexpr int kQ = 4;      // ring depth of row partials / factors handed between roles (>= LA + 2)
 constexpr int kMail = 32;  // batch picks a group leader publishes ahead of its followers
 constexpr unsigned long long kNoRow = ~0ull;  // ring slot sentinel: no batch left
@@ -598,6 +599,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     // Keeps every free ring slot loading; stores a batch as soon as its sweep 2
     // is done and refills the slot once the bulk engine has read it.
     if (lane != 0) return;
+    const unsigned t_start = static_cast<unsigned>(globaltimer_ns());
     const uint64_t pol = a.evict_first ? policy_evict_first() : policy_evict_normal();
     const unsigned long long nbt = (a.rows + B - 1) / B;  // batches of the whole matrix
     const unsigned long long mtag = static_cast<unsigned long long>(ctl->sweep_seq) << 32;
@@ -695,8 +697,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     }
     if (!SEED) bulk_wait<0>();  // every store landed before the CTA retires
     if (a.dbg) {
-      a.dbg[2 * cta] = smid();
-      a.dbg[2 * cta + 1] = nb;
+      a.dbg[kDbg * cta] = smid();
+      a.dbg[kDbg * cta + 1] = nb;
+      a.dbg[kDbg * cta + 2] = t_start;
+      a.dbg[kDbg * cta + 3] = static_cast<unsigned>(globaltimer_ns());
     }
 #ifdef UOT_TRACE
     atomicAdd(&uot_trace[8], clock64() - tr_p0);

@@ -230,7 +230,7 @@ struct uot_ctx {
   bool pinned = false;              // one sweep CTA on every SM: CTA slot = %smid (d_slot)
   unsigned* d_slot = nullptr;       // [sms] CTA slot of each SM (identity)
   unsigned long long* d_gbounds = nullptr;  // [groups+1] weighted static row blocks (UOT_SCHEDULE_WEIGHTED)
-  unsigned* d_dbg = nullptr;        // [grid][2] {smid, batches} of the last sweep
+  unsigned* d_dbg = nullptr;        // [grid][kDbg] {smid, batches, start, end} of the last sweep
   std::vector<uint32_t> weights;    // per row group (UOT_SCHEDULE_WEIGHTED)
   ulonglong2* mail = nullptr;  // [groups][kMail] batch picks of the group leaders
   // resident mode: the whole uot_iterate call is one persistent launch
@@ -451,8 +451,8 @@ int alloc_all(uot_ctx* ctx) {
   if ((rc = dalloc(ctx, &ctx->xrec, xn))) return rc;
   const size_t mn = static_cast<size_t>(ctx->grid) * kMail;  // >= groups * kMail
   if ((rc = dalloc(ctx, &ctx->mail, mn))) return rc;
-  if ((rc = dalloc(ctx, &ctx->d_dbg, 2 * static_cast<size_t>(ctx->grid)))) return rc;
-  CK(cudaMemsetAsync(ctx->d_dbg, 0, 2 * sizeof(unsigned) * ctx->grid, ctx->stream));
+  if ((rc = dalloc(ctx, &ctx->d_dbg, kDbg * static_cast<size_t>(ctx->grid)))) return rc;
+  CK(cudaMemsetAsync(ctx->d_dbg, 0, kDbg * sizeof(unsigned) * ctx->grid, ctx->stream));
   if (ctx->pinned) {
     std::vector<unsigned> slot(ctx->sms);
     for (int i = 0; i < ctx->sms; ++i) slot[i] = static_cast<unsigned>(i);
@@ -986,12 +986,12 @@ int uot_get_schedule_stats(const uot_ctx* cctx, uint32_t* cta_smid, uint32_t* ct
   auto* ctx = const_cast<uot_ctx*>(cctx);
   if (!ctx) return UOT_INVALID_PARAMETER;
   CK(cudaSetDevice(ctx->device));
-  std::vector<unsigned> h(2 * static_cast<size_t>(ctx->grid));
+  std::vector<unsigned> h(kDbg * static_cast<size_t>(ctx->grid));
   CK(cudaMemcpyAsync(h.data(), ctx->d_dbg, sizeof(unsigned) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   for (unsigned c = 0; c < ctx->grid; ++c) {
-    if (cta_smid) cta_smid[c] = h[2 * c];
-    if (cta_batches) cta_batches[c] = h[2 * c + 1];
+    if (cta_smid) cta_smid[c] = h[kDbg * c];
+    if (cta_batches) cta_batches[c] = h[kDbg * c + 1];
   }
   if (group_weight)
     for (unsigned g = 0; g < ctx->groups; ++g)
@@ -999,11 +999,18 @@ int uot_get_schedule_stats(const uot_ctx* cctx, uint32_t* cta_smid, uint32_t* ct
   return UOT_OK;
 }
 
-// Calibration of the weighted schedule: `k` dynamic iterations on a scratch
-// copy of the plan (the session's plan, factors, column sums and stop state are
-// untouched; only never-reset exchange tags advance), the row batches each
-// group took become its weight. Deterministic afterwards: the weights are
-// fixed, so every later solve with them is bit-reproducible.
+// Calibration of the weighted schedule, on a scratch copy of the plan (the
+// session's plan, factors, column sums and stop state are untouched; only
+// never-reset exchange tags advance):
+//   1. `k` dynamic iterations: the row batches each group took are its first
+//      weight (the per-SM HBM rates the dynamic counter adapts to);
+//   2. kRefineRounds rounds of two iterations under the weighted schedule
+//      itself: each group's completion time (its CTAs' last store, from the
+//      earliest CTA start) rescales its weight by (mean time / its time)^0.75,
+//      so the static blocks finish together as the dynamic batches do.
+// Deterministic afterwards: the weights are fixed, so every later solve with
+// them is bit-reproducible.
+constexpr int kRefineRounds = 3;  // (measured: 6 or 10 rounds, or an undamped update, are no better)
 int uot_calibrate_schedule(uot_ctx* ctx, uint32_t k) {
   if (!ctx) return UOT_INVALID_PARAMETER;
   if (!ctx->have_problem || !ctx->seeded)
@@ -1034,19 +1041,53 @@ int uot_calibrate_schedule(uot_ctx* ctx, uint32_t k) {
   void* real = ctx->P;
   const int sched = ctx->schedule, dyn = ctx->dyn;
   std::vector<uint64_t> counts(ctx->groups, 0);
+  std::vector<double> wd(ctx->groups, 1.0);
+  auto to_weights = [&]() {  // integer weights in [1, 2^19] proportional to wd
+    double m = 0.0;
+    for (double x : wd) m = std::max(m, x);
+    std::vector<uint32_t> w(ctx->groups);
+    for (unsigned g = 0; g < ctx->groups; ++g)
+      w[g] = static_cast<uint32_t>(std::max(1.0, std::min(double(1u << 19), std::round(wd[g] / m * (1u << 19)))));
+    return w;
+  };
   if (!rc) {
     ctx->P = scratch;
     ctx->schedule = UOT_SCHEDULE_DYNAMIC;
     ctx->dyn = 1;
     begin_iterate_kernel<<<1, 1, 0, ctx->stream>>>(ctx->ctl, 1e-300);
-    std::vector<unsigned> h(2 * static_cast<size_t>(ctx->grid));
-    for (uint32_t i = 0; i < k && !rc; ++i) {
+    std::vector<unsigned> h(kDbg * static_cast<size_t>(ctx->grid));
+    auto one_iteration = [&]() {
       rc = launch_sweep(ctx, false);
       if (!rc) rc = launch_finalize_single<kFinIter>(ctx);  // local finalize: no peer exchange for a scratch run
       if (!rc) rc = ctx->cuda(cudaMemcpyAsync(h.data(), ctx->d_dbg, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream), "copy");
       if (!rc) rc = ctx->cuda(cudaStreamSynchronize(ctx->stream), "calibration sweep");
+    };
+    for (uint32_t i = 0; i < k && !rc; ++i) {
+      one_iteration();
       if (i == 0) continue;  // warm-up
-      for (unsigned g = 0; g < ctx->groups && !rc; ++g) counts[g] += h[2 * (g * ctx->G) + 1];
+      for (unsigned g = 0; g < ctx->groups && !rc; ++g) counts[g] += h[kDbg * (g * ctx->G) + 1];
+    }
+    for (unsigned g = 0; g < ctx->groups; ++g) wd[g] = static_cast<double>(std::max<uint64_t>(1, counts[g]));
+    ctx->schedule = UOT_SCHEDULE_WEIGHTED;
+    ctx->dyn = 0;
+    for (int round = 0; round < kRefineRounds && !rc; ++round) {
+      const auto b = weighted_bounds(ctx->rows, to_weights());
+      rc = ctx->cuda(cudaMemcpyAsync(ctx->d_gbounds, b.data(), sizeof(unsigned long long) * b.size(),
+                                     cudaMemcpyHostToDevice, ctx->stream), "copy");
+      for (int i = 0; i < 2 && !rc; ++i) one_iteration();  // the second one is measured
+      if (rc) break;
+      unsigned t0 = h[2];
+      for (unsigned c = 1; c < ctx->grid; ++c)
+        if (static_cast<int>(h[kDbg * c + 2] - t0) < 0) t0 = h[kDbg * c + 2];
+      std::vector<double> tg(ctx->groups, 0.0);
+      double tmean = 0.0;
+      for (unsigned g = 0; g < ctx->groups; ++g) {
+        for (unsigned c = g * ctx->G; c < (g + 1) * ctx->G; ++c)
+          tg[g] = std::max(tg[g], static_cast<double>(static_cast<int>(h[kDbg * c + 3] - t0)));
+        tg[g] = std::max(tg[g], 1.0);
+        tmean += tg[g] / ctx->groups;
+      }
+      for (unsigned g = 0; g < ctx->groups; ++g) wd[g] *= std::pow(tmean / tg[g], 0.75);
     }
     ctx->P = real;
     ctx->schedule = sched;
@@ -1064,9 +1105,7 @@ int uot_calibrate_schedule(uot_ctx* ctx, uint32_t k) {
   if (saved) cudaFree(saved);
   if (rc) return rc;
   if ((rc = sync_ctl(ctx))) return rc;
-  std::vector<uint32_t> w(ctx->groups);
-  for (unsigned g = 0; g < ctx->groups; ++g)
-    w[g] = static_cast<uint32_t>(std::min<uint64_t>(1u << 20, std::max<uint64_t>(1, counts[g])));
+  const auto w = to_weights();
   return uot_set_group_weights(ctx, w.data(), ctx->groups);
 }
 
