@@ -77,6 +77,8 @@ typedef struct uot_layout {
   int32_t pinned;        /* one sweep CTA on every SM, slot = SM id (the weighted schedule is available) */
   int32_t variant;       /* iteration schedule (UOT_VARIANT_*); rows wider than #SMs slices (G > #SMs,
                             > 1.2M fp32 columns on a B200) run UOT_VARIANT_TWO_PASS, the only one they allow */
+  uint32_t keep_batches; /* static schedules of a streaming problem: each CTA stores its last keep_batches
+                            batches L2-resident and the next sweep walks its row block the other way */
 } uot_layout;
 
 /* ---- sessions ---------------------------------------------------------- */

@@ -65,6 +65,8 @@ struct SweepArgs {
   const unsigned long long* gbounds;  // [groups+1] static row block of each group, or nullptr (balanced)
   unsigned* dbg;              // [grid][kDbg] {smid, batches, start, end ns} of the last sweep (schedule statistics)
   int dyn;                    // batches handed out by a global counter (else a static row block)
+  unsigned keep;              // static blocks: a CTA stores its last `keep` batches L2-resident (evict_last)
+                              // and walks its block in alternating directions, so the next sweep starts on them
   ulonglong2* mail;           // [groups][kMail] {first row, tag}: the group leader's batch picks (dyn, G > 1)
   double fi;
 };
@@ -601,6 +603,13 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     if (lane != 0) return;
     const unsigned t_start = static_cast<unsigned>(globaltimer_ns());
     const uint64_t pol = a.evict_first ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_keep = policy_evict_last();
+    // Iteration t = iter + 1 walks a static block backwards when t is odd: it
+    // starts on the batches iteration t-1 (or the forward seed sweep) stored
+    // last, still in L2 — their reads hit and their previous writes are
+    // overwritten before reaching HBM.
+    const bool snake = a.keep > 0 && !a.dyn && !SEED;
+    const bool back = snake && ((ctl->iter + 1) & 1ull);
     const unsigned long long nbt = (a.rows + B - 1) / B;  // batches of the whole matrix
     const unsigned long long mtag = static_cast<unsigned long long>(ctl->sweep_seq) << 32;
     ulonglong2* mail = a.mail + static_cast<size_t>(group) * kMail;
@@ -612,8 +621,16 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       // (the seed sweep has no row exchange to bound how far a leader runs
       // ahead of its followers, so with G > 1 it keeps the static blocks)
       if (!a.dyn || (SEED && G > 1)) {
-        row = b < nb_static ? r0 + static_cast<unsigned long long>(b) * B : kNoRow;
-        if (row != kNoRow) row |= min(static_cast<unsigned long long>(B), r1 - row) << 56;
+        if (b >= nb_static) {
+          row = kNoRow;
+        } else if (back) {  // batch b covers [max(r0, hi - B), hi), hi = r1 - b*B (rows ascending inside)
+          const unsigned long long hi = r1 - static_cast<unsigned long long>(b) * B;
+          const unsigned long long lo = hi > r0 + B ? hi - B : r0;
+          row = lo | ((hi - lo) << 56);
+        } else {
+          row = r0 + static_cast<unsigned long long>(b) * B;
+          row |= min(static_cast<unsigned long long>(B), r1 - row) << 56;
+        }
       } else if (G == 1 || g == 0) {
         const unsigned long long t = atomicAdd(&ctl->batch_next, 1ull);
         row = t < nbt ? t * B : kNoRow;
@@ -666,11 +683,12 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       const unsigned nr = rows_at(row);
       const T* srcs = slot_ptr(b);
       T* dst = gbase + row_of(row) * a.pitch;
+      const uint64_t sp = snake && b + a.keep >= nb_static ? pol_keep : pol;
       if (G == 1) {
-        bulk_s2g(dst, srcs, nr * row_bytes, pol);
+        bulk_s2g(dst, srcs, nr * row_bytes, sp);
       } else {
         for (unsigned r = 0; r < nr; ++r)
-          bulk_s2g(dst + static_cast<size_t>(r) * a.pitch, srcs + r * a.slice, row_bytes, pol);
+          bulk_s2g(dst + static_cast<size_t>(r) * a.pitch, srcs + r * a.slice, row_bytes, sp);
       }
       bulk_commit();
     };

@@ -51,6 +51,11 @@ struct SweepCfg {
 // more issue slots than they buy).
 // (Measured: a lag of 3 for G > 1 — more slack between a group's CTAs — is
 // 10-15% slower: the 7-slot ring then prefetches only two batches.)
+// L2 bytes (all CTAs together) written evict_last at the end of a streaming sweep
+// and read first by the next one (measured 48, 64, 88 MiB: 48 MiB best at 8192^2,
+// -3% per iteration; +-0 at the HBM-sized configs; the 126 MB L2 also holds the
+// column partials and the stream's own lines).
+constexpr uint64_t kKeepL2Bytes = 48ull << 20;
 constexpr int kLag = 2;
 constexpr int kLagX = 2;
 constexpr int kFactorWarpsG1 = 3;
@@ -223,6 +228,7 @@ struct uot_ctx {
   size_t smem = 0;
   const SweepCfg* cfg = nullptr;
   int evict_first = 0;
+  unsigned keep = 0;  // batches per CTA stored L2-resident for the next sweep (SweepArgs::keep)
   int full = 0;
   int smid_map = 0;
   int dyn = 1;  // batches handed out by a global counter (SweepArgs::dyn)
@@ -389,6 +395,11 @@ int plan_layout(uot_ctx* ctx) {
   int smem_optin = 0;
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   ctx->evict_first = static_cast<uint64_t>(ctx->rows) * ctx->pitch * ctx->esz > (64ull << 20) ? 1 : 0;
+  // Streaming problems keep the last kKeepL2Bytes of every CTA's sweep in L2 for
+  // the next sweep, which walks the blocks the other way (SweepArgs::keep).
+  ctx->keep = ctx->evict_first
+                  ? static_cast<unsigned>(kKeepL2Bytes / (static_cast<uint64_t>(ctx->grid) * ctx->B * slice * ctx->esz))
+                  : 0u;
   // Row-batch schedule: fixed row blocks (bit-reproducible run to run, as the
   // reference's ordered reduction) unless the caller opts into the dynamic
   // batch counter with uot_set_deterministic(ctx, 0).
@@ -508,6 +519,7 @@ SweepArgs sweep_args(const uot_ctx* ctx) {
   a.evict_first = ctx->evict_first;
   a.smid_map = ctx->smid_map;
   a.dyn = ctx->dyn;
+  a.keep = ctx->keep;
   a.slot_of_sm = ctx->pinned ? ctx->d_slot : nullptr;
   a.gbounds = ctx->pinned && ctx->schedule == UOT_SCHEDULE_WEIGHTED ? ctx->d_gbounds : nullptr;
   a.dbg = ctx->d_dbg;
@@ -1201,6 +1213,7 @@ int uot_get_layout(const uot_ctx* ctx, uot_layout* o) {
   o->smid_map = ctx->smid_map;
   o->exchange = ctx->xmode;
   o->variant = ctx->variant;
+  o->keep_batches = ctx->dyn ? 0u : ctx->keep;
   return UOT_OK;
 }
 

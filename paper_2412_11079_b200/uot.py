@@ -91,7 +91,7 @@ class Layout(C.Structure):
                 ("smid_map", C.c_int32), ("exchange", C.c_int32),
                 ("resident", C.c_int32), ("dtype", C.c_int32),
                 ("dynamic", C.c_int32), ("schedule", C.c_int32), ("pinned", C.c_int32),
-                ("variant", C.c_int32)]
+                ("variant", C.c_int32), ("keep_batches", C.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

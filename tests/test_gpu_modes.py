@@ -24,7 +24,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run(uot, a, rpd, cpd, er, ep, k, tol=KNEVER, resident=True, chunks=None, deterministic=True):
-    with uot.Session(a.shape[0], a.shape[1]) as s:
+    with uot.Session(a.shape[0], a.shape[1], dtype=a.dtype) as s:
         s.set_resident(resident)
         s.set_deterministic(deterministic)
         lay = s.layout
@@ -118,6 +118,28 @@ def test_batch_schedules(gpu, orc, m, n, k):
         assert np.array_equal(out[x][0], out[y][0])
         np.testing.assert_array_equal(out[x][1].alpha, out[y][1].alpha)
         np.testing.assert_array_equal(out[x][2], out[y][2])
+
+
+@pytest.mark.parametrize("m,n,dt", [(4099, 8192, np.float32), (3001, 8200, np.float32), (2100, 4100, np.float64)])
+def test_alternating_sweeps_keep_rows_in_l2(gpu, orc, m, n, dt):
+    """Streaming problems (> 64 MiB) store each CTA's last batches L2-resident and
+    walk the static row blocks in alternating directions (SweepArgs::keep): the
+    direction follows the iteration count, so k iterations in one call, in
+    single-iteration calls, or across a resume give the same bits, and every
+    count meets the parity bar (odd and even: the backward sweep is the last)."""
+    a, rpd, cpd = orc.gen_problem(21, m, n, dtype=dt)
+    for k in (3, 4):
+        ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, k, 4)
+        plans = []
+        for chunks in ([k], [1] * k, [2, k - 2]):
+            p, f, cs, done, err, conv, lay = run(gpu, a, rpd, cpd, 1.0, 0.1, k, chunks=chunks)
+            assert done == k and lay["keep_batches"] > 0 and lay["evict_first"] == 1
+            plans.append((p, f.alpha, f.beta, cs))
+        assert_parity(plans[0][0], ref.plan, rpd, cpd, f"{m}x{n} {np.dtype(dt).name} K={k}")
+        np.testing.assert_allclose(plans[0][1], ref.alpha, rtol=1e-10)
+        for other in plans[1:]:
+            for x, y in zip(plans[0], other):
+                assert np.array_equal(x, y)
 
 
 @pytest.mark.slow

@@ -81,7 +81,7 @@ def main():
         for lib in libs:
             env = dict(os.environ, UOT_LIB_PATH=os.path.abspath(lib), UOT_AUTOBUILD="0")
             p = subprocess.run([sys.executable, os.path.abspath(__file__), "--inner", *passthru], env=env,
-                               capture_output=True, text=True, timeout=1200)
+                               capture_output=True, text=True, timeout=int(arg("--proc-timeout", 1200)))
             line = next((x for x in p.stdout.splitlines() if x.startswith("JSON")), None)
             if line is None:
                 print(f"{lib}: failed\n{p.stdout[-2000:]}\n{p.stderr[-2000:]}", flush=True)
