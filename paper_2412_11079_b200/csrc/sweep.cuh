@@ -22,11 +22,18 @@
 //     into row factors. NW compute warps do the arithmetic.
 //   * Compute warps never meet a CTA-wide barrier: they wait only for data
 //     (full) and factors (alpha_rdy) and hand work on through mbarriers (done1:
-//     row partials written; done2: sweep 2 finished). Step s runs sweep 1 of
-//     batch s, then sweep 2 of batch s-LA-1, then the row reduction of batch s.
-//   * Per-column state lives in registers of the owning thread: beta_j (f64)
-//     and the column partial next_j (f64). Thread t owns float4 chunks
-//     t, t+NT, ... of the slice (conflict-free 128-bit smem access).
+//     row partials written; done2: sweep 2 finished).
+//     Wide one-row slices (V >= 3, factors in TMEM): SPLIT roles — half the
+//     compute warps run sweep 1 + the row partials of every batch as soon as it
+//     lands (paced by the ring only), the other half sweep 2 + the column
+//     partials once the batch's factor is published; each thread covers 2V
+//     chunks, each warp waits on one barrier per batch (measured -2% at 32768^2
+//     and 131072x32768, -4% at 8192^2 against both sweeps in every warp).
+//     Other slices: step s runs sweep 1 of batch s, then sweep 2 of batch
+//     s-LA-1, then the row reduction of batch s, in every compute warp.
+//   * Per-column state of the owning thread: beta_j (f64, registers or TMEM)
+//     and the column partial next_j (f64, registers). Thread t owns float4
+//     chunks t, t+NT, ... of the slice (conflict-free 128-bit smem access).
 //   * Row sums: thread partial -> warp xor-tree -> per-warp smem -> factor lane
 //     sums the NW warp partials in warp order. With G > 1 the G CTA partials of
 //     a row are exchanged through L2 as 128-bit single-copy-atomic {value, tag}
@@ -97,9 +104,10 @@ __host__ __device__ constexpr int tr_slot(int id) {
 #define TR_FLUSH(lo, hi)
 #endif
 
-constexpr int kRing = 8;   // exchange records per CTA
+constexpr int kRing = 16;  // exchange records per CTA (> how far a CTA's factor warps can run ahead of a peer's)
 constexpr int kDbg = 4;    // schedule statistics per CTA: SM id, row batches, producer start / end (globaltimer ns, low 32 bits)
 constexpr int kQ = 4;      // ring depth of row partials / factors handed between roles (>= LA + 2)
+constexpr int kQMax = 12;  // smem reserved for the row-partial / factor rings (split roles: > NBUF, multiple of NF)
 constexpr int kMail = 32;  // batch picks a group leader publishes ahead of its followers
 constexpr unsigned long long kNoRow = ~0ull;  // ring slot sentinel: no batch left
 
@@ -367,10 +375,10 @@ __device__ __forceinline__ void tmem_fence_after_() { asm volatile("tcgen05.fenc
 
 // Sweep 1 with the factors of each chunk group loaded from TMEM (tcol: this
 // thread's first factor column).
-template <int NT, int V, bool FULL>
+template <int NT, int V, bool FULL, int KG0 = ChunkGroup<V>::KG>
 __device__ __forceinline__ double row_sweep1_tb(float4* row, unsigned tid, unsigned nq, uint32_t tcol,
                                                 ScreenBounds sb, bool& bad) {
-  constexpr int KG = ChunkGroup<V>::KG;  // (KG = 4 measured slower: it spills again)
+  constexpr int KG = KG0;  // (KG = 4 measured slower with both sweeps in one warp: it spills)
   double s[4];
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
@@ -391,10 +399,10 @@ __device__ __forceinline__ double row_sweep1_tb(float4* row, unsigned tid, unsig
 
 // Sweep 2 of this thread's part of one row. `exact`: one of the thread's
 // chunk groups of the row took the exact path in sweep 1.
-template <int NT, int V, bool FULL>
+template <int NT, int V, bool FULL, int KG0 = ChunkGroup<V>::KG>
 __device__ __forceinline__ void row_sweep2(float4* row, unsigned tid, unsigned nq, double al, bool exact,
                                            double* acc) {
-  constexpr int KG = ChunkGroup<V>::KG;
+  constexpr int KG = KG0;
   exact = exact || !(al >= 1.0 / kAlphaMargin && al <= kAlphaMargin);
 #pragma unroll
   for (int g0 = 0; g0 < V; g0 += KG) {
@@ -498,9 +506,10 @@ constexpr int elems_per_chunk() {
 // Shared-memory layout shared by host sizing and the kernel.
 template <int NW, int BM, int NBUF>
 struct SweepSmem {
-  static constexpr int kBars = NBUF /*full*/ + NBUF /*done2*/ + kQ /*done1*/ + kQ /*alpha_rdy*/;
-  static constexpr int kDoubles = kQ * NW * BM /*red*/ + kQ * BM /*alpha*/ + NBUF /*first row of each slot*/ +
-                                  1 /*TMEM base*/;
+  static constexpr int kQS = BM == 1 ? kQMax : kQ;  // ring slots reserved (split roles: one-row batches)
+  static constexpr int kBars = NBUF /*full*/ + NBUF /*done2*/ + kQS /*done1*/ + kQS /*alpha_rdy*/;
+  static constexpr int kDoubles = kQS * NW * BM /*red*/ + kQS * BM /*alpha*/ + NBUF /*first row of each slot*/ +
+                                  1 /*TMEM base*/ + kQS * NW / 2 /*exact-path flags (u32)*/;
   static size_t bytes(unsigned buf_stride) {
     return static_cast<size_t>(NBUF) * buf_stride + kBars * 8 + kDoubles * 8;
   }
@@ -519,6 +528,14 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   constexpr bool F64 = std::is_same<T, double>::value;
   constexpr bool TB = TB0 && !F64 && !SEED && NW % 4 == 0;  // column factors in TMEM
   constexpr int kTbCols = (8 * V * (NW / 4) <= 32) ? 32 : (8 * V * (NW / 4) <= 64) ? 64 : (8 * V * (NW / 4) <= 128) ? 128 : 256;
+  // Split roles: half the compute warps run sweep 1 (and the row sums) over the
+  // whole slice, the other half sweep 2 (and the column sums); sweep-1 warps are
+  // paced by the ring only, so the row-partial / factor rings hold QD > NBUF
+  // batches (a multiple of NF: each ring slot is served by one factor warp).
+  constexpr bool SPLIT = TB && BM == 1 && NW % 8 == 0;
+  constexpr int QD = SPLIT ? (NF == 3 ? 9 : 8) : kQ;
+  constexpr int NWR = SPLIT ? NW / 2 : NW;  // warps contributing row partials
+  static_assert(!SPLIT || (QD > NBUF && QD % NF == 0 && QD <= SweepSmem<NW, BM, NBUF>::kQS), "split-role rings");
   constexpr int EPC = elems_per_chunk<T>();  // 4 floats or 2 doubles per 16-byte chunk
   static_assert(NF >= 1 && NF <= kErrSlots, "factor warps");
   static_assert(LA >= 1 && LA + 2 <= kQ && (!XCHG || LA >= 2), "lag (the alpha / red rings hold kQ batches)");
@@ -539,13 +556,15 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NBUF * a.buf_stride);
   uint64_t* done2 = full + NBUF;
   uint64_t* done1 = done2 + NBUF;
-  uint64_t* alpha_rdy = done1 + kQ;
-  double* red = reinterpret_cast<double*>(alpha_rdy + kQ);  // [kQ][NW][BM]
-  double* alpha_s = red + kQ * NW * BM;                      // [kQ][BM]
+  constexpr int kQS = SweepSmem<NW, BM, NBUF>::kQS;
+  uint64_t* alpha_rdy = done1 + kQS;
+  double* red = reinterpret_cast<double*>(alpha_rdy + kQS);  // [QD][NWR][BM]
+  double* alpha_s = red + kQS * NW * BM;                      // [QD][BM]
   // first row of the batch in each ring slot (kNoRow: the CTA's batches are
   // exhausted), written by the producer before the slot's full barrier
-  unsigned long long* srow = reinterpret_cast<unsigned long long*>(alpha_s + kQ * BM);
+  unsigned long long* srow = reinterpret_cast<unsigned long long*>(alpha_s + kQS * BM);
   uint32_t* tmem_s = reinterpret_cast<uint32_t*>(srow + NBUF);  // TMEM base (TB)
+  uint32_t* xbad = tmem_s + 2;  // [QD][NWR] split roles: a sweep-1 warp took the exact path on the batch
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned G = a.G;
@@ -573,10 +592,10 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   if (tid == 0) {
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&done2[i], NW);
+      mbar_init(&done2[i], NWR);
     }
-    for (int i = 0; i < kQ; ++i) {
-      mbar_init(&done1[i], NW);
+    for (int i = 0; i < QD; ++i) {
+      mbar_init(&done1[i], NWR);
       mbar_init(&alpha_rdy[i], 1);
     }
     fence_mbar_init();
@@ -744,20 +763,25 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
       // the slot's first row (the slot cannot be refilled before this warp's alpha)
       mbar_wait(&full[s % NBUF], (s / NBUF) & 1u);
       const unsigned long long packed = srow[s % NBUF];
-      if (packed == kNoRow) break;
+      if (packed == kNoRow) {
+        // split roles: the sweep-2 warps learn the end from the factor ring (each
+        // factor warp's first sentinel completes its slot's phase; only batch nb's is awaited)
+        if (SPLIT && lane == 0) mbar_arrive(&alpha_rdy[s % QD]);
+        break;
+      }
       const unsigned nr = rows_at(packed);
       const unsigned long long row = row_of(packed);
-      const unsigned q = s % kQ;
+      const unsigned q = s % QD;
       double rv = 0.0;
       if (lane < static_cast<int>(nr)) rv = __ldg(&a.rpd[row + lane]);
       TR_BEGIN();
-      mbar_wait(&done1[q], (s / kQ) & 1u);
+      mbar_wait(&done1[q], (s / QD) & 1u);
       TR_END(0);
       double t = 0.0;  // this CTA's partial of row `lane` of the batch, warp order
       if (lane < static_cast<int>(nr)) {
-        t = red[(q * NW) * BM + lane];
+        t = red[(q * NWR) * BM + lane];
 #pragma unroll
-        for (int w = 1; w < NW; ++w) t += red[(q * NW + w) * BM + lane];
+        for (int w = 1; w < NWR; ++w) t += red[(q * NWR + w) * BM + lane];
       }
       if (XCHG) {
         TR_BEGIN();
@@ -804,6 +828,82 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   }
 
   // ========================================================= compute warps ==
+  if constexpr (SPLIT) {
+    // Split roles. Threads [0, NT/2): sweep 1 of every batch over the whole
+    // slice (chunks t + k*NT/2, k < 2V; factors in TMEM), the row partials and
+    // an exact-path flag per warp. Threads [NT/2, NT): sweep 2 of every batch
+    // once its factor is published, and the column partials. Each warp waits on
+    // one barrier per batch and keeps twice the independent work per wait.
+    constexpr int NT2 = NT / 2, V2 = 2 * V, NW2 = NW / 2;
+    const bool sweep1_role = tid < NT2;
+    const unsigned t = sweep1_role ? tid : tid - NT2;
+    const unsigned w = t >> 5;
+    if (sweep1_role) {
+      ScreenBounds sb1;
+      const uint32_t tc = tbase + (static_cast<uint32_t>(32 * (w % 4)) << 16) + 8 * V2 * (w / 4);
+      {
+        double beta[4 * V2];
+        const double* bsrc = a.beta2 + ((ctl->iter + 1) & 1ull) * a.pitch + static_cast<size_t>(g) * a.slice;
+#pragma unroll
+        for (int k = 0; k < V2; ++k) {
+          const unsigned q = t + k * NT2;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) beta[4 * k + e] = (FULL || q < nq) ? bsrc[4 * q + e] : 1.0;
+        }
+        sb1 = screen_bounds(beta, 4 * V2);
+#pragma unroll
+        for (int k = 0; k < V2; ++k) tmem_st_chunk(tc + 8 * k, beta + 4 * k);
+        tmem_wait_st_();
+      }
+      for (unsigned s = 0;; ++s) {
+        const unsigned slot = s % NBUF;
+        mbar_wait(&full[slot], (s / NBUF) & 1u);
+        if (srow[slot] == kNoRow) break;
+        bool bad = false;
+        const double part = row_sweep1_tb<NT2, V2, FULL>(
+            reinterpret_cast<float4*>(smem + slot * a.buf_stride), t, nq, tc, sb1, bad);
+        const double ts = warp_sum(part);
+        const unsigned any_bad = __any_sync(0xffffffffu, bad);
+        const unsigned q = s % QD;
+        if (lane == 0) {
+          red[q * NW2 + w] = ts;
+          xbad[q * NW2 + w] = any_bad;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done1[q]);
+      }
+      tmem_fence_before_();
+      asm volatile("bar.sync 1, %0;" ::"n"(NT2) : "memory");
+      if (w == 0) {
+        tmem_fence_after_();
+        tmem_dealloc_cols<kTbCols>(tbase);
+      }
+    } else {
+      double acc2[4 * V2];
+#pragma unroll
+      for (int i = 0; i < 4 * V2; ++i) acc2[i] = 0.0;
+      for (unsigned b = 0;; ++b) {
+        const unsigned q = b % QD, slot = b % NBUF;
+        mbar_wait(&alpha_rdy[q], (b / QD) & 1u);
+        if (srow[slot] == kNoRow) break;  // (the factor warps' sentinel completed this phase)
+        row_sweep2<NT2, V2, FULL>(reinterpret_cast<float4*>(smem + slot * a.buf_stride), t, nq, alpha_s[q],
+                                  xbad[q * NW2 + w] != 0u, acc2);
+        fence_proxy_async_smem();  // generic writes -> the producer's bulk store
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done2[slot]);
+      }
+      double* dst = a.partials + static_cast<size_t>(group) * a.pitch + static_cast<size_t>(g) * a.slice;
+#pragma unroll
+      for (int k = 0; k < V2; ++k) {
+        const unsigned q = t + k * NT2;
+        if (q < nq) {
+          reinterpret_cast<double2*>(dst)[2 * q] = make_double2(acc2[4 * k], acc2[4 * k + 1]);
+          reinterpret_cast<double2*>(dst)[2 * q + 1] = make_double2(acc2[4 * k + 2], acc2[4 * k + 3]);
+        }
+      }
+    }
+    return;
+  } else {
   double beta[EPC * V], acc[EPC * V];
 #pragma unroll
   for (int i = 0; i < EPC * V; ++i) acc[i] = 0.0;
@@ -960,6 +1060,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
             make_double2(acc[EPC * k + 2 * h], acc[EPC * k + 2 * h + 1]);
     }
   }
+  }  // !SPLIT
 }
 
 }  // namespace uotk

@@ -25,7 +25,10 @@ def check(name, plan, ref):
 
 # streaming G=1 (34 rows per CTA: not resident), G=3, G=4 with TMEM column
 # factors, resident, tiny
-cases = [(5100, 1000, 3), (24, 20000, 3), (40, 32768, 3), (96, 1000, 5), (7, 9, 3)]
+# streaming G=1 with wide slices (split sweep roles) and a problem past the 64 MiB
+# L2-keep threshold (alternating sweep directions)
+cases = [(5100, 1000, 3), (24, 20000, 3), (40, 32768, 3), (96, 1000, 5), (7, 9, 3), (400, 8192, 3),
+         (2100, 8192, 3)]
 for m, n, k in cases:
     a, rpd, cpd = o.gen_problem(42, m, n)
     ref = o.fused_solve(a, rpd, cpd, 1.0, 0.1, KN, k, workers=2)
