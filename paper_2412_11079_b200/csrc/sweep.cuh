@@ -497,6 +497,65 @@ __device__ __forceinline__ void row_seed_f64(const double2* row, unsigned tid, u
   }
 }
 
+// Row batches of one CTA's sweep (the producer's schedule), as {first row, rows}
+// packed into 64 bits (rows in the top byte), or kNoRow once the CTA's batches
+// are exhausted (pick.nb = the local batch count from then on). Static: the
+// group's contiguous block [r0, r1) (balanced_blocks, plan.cpp:11-21, or the
+// weighted bounds), walked backwards when `back`. Dynamic: batches of B rows
+// from a global counter (ctl->batch_next), so faster SMs take more of them —
+// per-SM HBM bandwidth on B200 differs by up to 2x with the GPC an SM sits in
+// (tools/microbench/stream_bench.cu); with G > 1 the group leader picks and
+// publishes its pick to the followers through the group's mailbox ring.
+struct BatchPick {
+  Control* ctl;
+  ulonglong2* mail;                   // this group's [kMail] ring
+  unsigned long long r0, r1, nbt, mtag, rows;
+  unsigned B, G, g, nb_static;
+  bool dyn, back;
+  unsigned nb = 0xffffffffu;
+  __device__ unsigned long long operator()(unsigned b) {
+    if (b >= nb) return kNoRow;
+    unsigned long long row;
+    if (!dyn) {
+      if (b >= nb_static) {
+        row = kNoRow;
+      } else if (back) {  // batch b covers [max(r0, hi - B), hi), hi = r1 - b*B (rows ascending inside)
+        const unsigned long long hi = r1 - static_cast<unsigned long long>(b) * B;
+        const unsigned long long lo = hi > r0 + B ? hi - B : r0;
+        row = lo | ((hi - lo) << 56);
+      } else {
+        row = r0 + static_cast<unsigned long long>(b) * B;
+        row |= min(static_cast<unsigned long long>(B), r1 - row) << 56;
+      }
+    } else if (G == 1 || g == 0) {
+      const unsigned long long t = atomicAdd(&ctl->batch_next, 1ull);
+      row = t < nbt ? t * B : kNoRow;
+      if (row != kNoRow) row |= min(static_cast<unsigned long long>(B), rows - row) << 56;
+      if (G > 1) st_relaxed_b128(&mail[b % kMail], row, mtag | (b + 1));
+    } else {
+      unsigned long long lo, hi;
+      ld_relaxed_b128(&mail[b % kMail], lo, hi);
+      if (hi != (mtag | (b + 1))) {
+        const unsigned long long t0 = globaltimer_ns();
+        unsigned n = 0;
+        do {
+          ld_relaxed_b128(&mail[b % kMail], lo, hi);
+          if (hi != (mtag | (b + 1)) && (++n & 255u) == 0 && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
+            atomicOr(&ctl->status, kStatusExchangeTimeout);
+            lo = kNoRow;
+            break;
+          }
+        } while (hi != (mtag | (b + 1)));
+      }
+      row = lo;
+    }
+    if (row == kNoRow) nb = b;
+    return row;
+  }
+};
+__device__ __forceinline__ unsigned rows_of_batch(unsigned long long v) { return static_cast<unsigned>(v >> 56); }
+__device__ __forceinline__ unsigned long long row_of_batch(unsigned long long v) { return v & ((1ull << 56) - 1); }
+
 // Elements per 16-byte chunk of the storage type.
 template <typename T>
 constexpr int elems_per_chunk() {
@@ -629,55 +688,12 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     // overwritten before reaching HBM.
     const bool snake = a.keep > 0 && !a.dyn && !SEED;
     const bool back = snake && ((ctl->iter + 1) & 1ull);
-    const unsigned long long nbt = (a.rows + B - 1) / B;  // batches of the whole matrix
-    const unsigned long long mtag = static_cast<unsigned long long>(ctl->sweep_seq) << 32;
-    ulonglong2* mail = a.mail + static_cast<size_t>(group) * kMail;
-    unsigned nb = 0xffffffffu;  // local batches with rows (known at the first sentinel)
-    // first row of local batch b, or kNoRow
-    auto pick = [&](unsigned b) -> unsigned long long {
-      if (b >= nb) return kNoRow;
-      unsigned long long row;
-      // (the seed sweep has no row exchange to bound how far a leader runs
-      // ahead of its followers, so with G > 1 it keeps the static blocks)
-      if (!a.dyn || (SEED && G > 1)) {
-        if (b >= nb_static) {
-          row = kNoRow;
-        } else if (back) {  // batch b covers [max(r0, hi - B), hi), hi = r1 - b*B (rows ascending inside)
-          const unsigned long long hi = r1 - static_cast<unsigned long long>(b) * B;
-          const unsigned long long lo = hi > r0 + B ? hi - B : r0;
-          row = lo | ((hi - lo) << 56);
-        } else {
-          row = r0 + static_cast<unsigned long long>(b) * B;
-          row |= min(static_cast<unsigned long long>(B), r1 - row) << 56;
-        }
-      } else if (G == 1 || g == 0) {
-        const unsigned long long t = atomicAdd(&ctl->batch_next, 1ull);
-        row = t < nbt ? t * B : kNoRow;
-        if (row != kNoRow) row |= min(static_cast<unsigned long long>(B), a.rows - row) << 56;
-        if (G > 1) st_relaxed_b128(&mail[b % kMail], row, mtag | (b + 1));
-      } else {
-        unsigned long long lo, hi;
-        ld_relaxed_b128(&mail[b % kMail], lo, hi);
-        if (hi != (mtag | (b + 1))) {
-          const unsigned long long t0 = globaltimer_ns();
-          unsigned n = 0;
-          do {
-            ld_relaxed_b128(&mail[b % kMail], lo, hi);
-            if (hi != (mtag | (b + 1)) && (++n & 255u) == 0 && globaltimer_ns() - t0 > kExchangeTimeoutNs) {
-#ifdef UOT_DEBUG
-              printf("mail timeout cta %u group %u b %u want %llx seen %llx\n", cta, group, b, mtag | (b + 1), hi);
-#endif
-              atomicOr(&ctl->status, kStatusExchangeTimeout);
-              lo = kNoRow;
-              break;
-            }
-          } while (hi != (mtag | (b + 1)));
-        }
-        row = lo;
-      }
-      if (row == kNoRow) nb = b;
-      return row;
-    };
+    BatchPick pick{ctl, a.mail + static_cast<size_t>(group) * kMail, r0, r1, (a.rows + B - 1) / B,
+                   static_cast<unsigned long long>(ctl->sweep_seq) << 32, a.rows, B, G, g, nb_static,
+                   // (the seed sweep has no row exchange to bound how far a leader runs
+                   // ahead of its followers, so with G > 1 it keeps the static blocks)
+                   a.dyn && !(SEED && G > 1), back};
+    unsigned& nb = pick.nb;  // local batches with rows (known at the first sentinel)
     auto issue_load = [&](unsigned b) {
       const unsigned long long row = pick(b);
       uint64_t* bar = &full[b % NBUF];
