@@ -23,12 +23,13 @@
 //   * Compute warps never meet a CTA-wide barrier: they wait only for data
 //     (full) and factors (alpha_rdy) and hand work on through mbarriers (done1:
 //     row partials written; done2: sweep 2 finished).
-//     Wide one-row slices (V >= 3, factors in TMEM): SPLIT roles — half the
-//     compute warps run sweep 1 + the row partials of every batch as soon as it
-//     lands (paced by the ring only), the other half sweep 2 + the column
-//     partials once the batch's factor is published; each thread covers 2V
-//     chunks, each warp waits on one barrier per batch (measured -2% at 32768^2
-//     and 131072x32768, -4% at 8192^2 against both sweeps in every warp).
+//     Slices of V >= 2 float4 per thread, batches of <= 2 rows: SPLIT roles —
+//     half the compute warps run sweep 1 + the row partials of every batch as
+//     soon as it lands (paced by the ring only), the other half sweep 2 + the
+//     column partials once the batch's factors are published; each thread
+//     covers 2V chunks, each warp waits on one barrier per batch (measured -2%
+//     at 32768^2, 131072x32768 and 262144x4096, -4% at 8192^2 against both
+//     sweeps in every warp).
 //     Other slices: step s runs sweep 1 of batch s, then sweep 2 of batch
 //     s-LA-1, then the row reduction of batch s, in every compute warp.
 //   * Per-column state of the owning thread: beta_j (f64, registers or TMEM)
@@ -565,10 +566,11 @@ constexpr int elems_per_chunk() {
 // Shared-memory layout shared by host sizing and the kernel.
 template <int NW, int BM, int NBUF>
 struct SweepSmem {
-  static constexpr int kQS = BM == 1 ? kQMax : kQ;  // ring slots reserved (split roles: one-row batches)
+  static constexpr int kQS = BM <= 2 ? kQMax : kQ;  // ring slots reserved (split roles: batches of <= 2 rows)
+  static constexpr int kRed = kQ * NW * BM > kQS * (NW / 2) * BM ? kQ * NW * BM : kQS * (NW / 2) * BM;
   static constexpr int kBars = NBUF /*full*/ + NBUF /*done2*/ + kQS /*done1*/ + kQS /*alpha_rdy*/;
-  static constexpr int kDoubles = kQS * NW * BM /*red*/ + kQS * BM /*alpha*/ + NBUF /*first row of each slot*/ +
-                                  1 /*TMEM base*/ + kQS * NW / 2 /*exact-path flags (u32)*/;
+  static constexpr int kDoubles = kRed /*red*/ + kQS * BM /*alpha*/ + NBUF /*first row of each slot*/ +
+                                  1 /*TMEM base*/ + kQS * NW / 4 /*exact-path masks (u32, [kQS][NW/2])*/;
   static size_t bytes(unsigned buf_stride) {
     return static_cast<size_t>(NBUF) * buf_stride + kBars * 8 + kDoubles * 8;
   }
@@ -591,7 +593,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   // whole slice, the other half sweep 2 (and the column sums); sweep-1 warps are
   // paced by the ring only, so the row-partial / factor rings hold QD > NBUF
   // batches (a multiple of NF: each ring slot is served by one factor warp).
-  constexpr bool SPLIT = TB && BM == 1 && NW % 8 == 0;
+  constexpr bool SPLIT = !SEED && !F64 && NW % 8 == 0 && BM <= 2 && (TB || V == 2);
   constexpr int QD = SPLIT ? (NF == 3 ? 9 : 8) : kQ;
   constexpr int NWR = SPLIT ? NW / 2 : NW;  // warps contributing row partials
   static_assert(!SPLIT || (QD > NBUF && QD % NF == 0 && QD <= SweepSmem<NW, BM, NBUF>::kQS), "split-role rings");
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   constexpr int kQS = SweepSmem<NW, BM, NBUF>::kQS;
   uint64_t* alpha_rdy = done1 + kQS;
   double* red = reinterpret_cast<double*>(alpha_rdy + kQS);  // [QD][NWR][BM]
-  double* alpha_s = red + kQS * NW * BM;                      // [QD][BM]
+  double* alpha_s = red + SweepSmem<NW, BM, NBUF>::kRed;      // [QD][BM]
   // first row of the batch in each ring slot (kNoRow: the CTA's batches are
   // exhausted), written by the producer before the slot's full barrier
   unsigned long long* srow = reinterpret_cast<unsigned long long*>(alpha_s + kQS * BM);
@@ -846,10 +848,11 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
   // ========================================================= compute warps ==
   if constexpr (SPLIT) {
     // Split roles. Threads [0, NT/2): sweep 1 of every batch over the whole
-    // slice (chunks t + k*NT/2, k < 2V; factors in TMEM), the row partials and
-    // an exact-path flag per warp. Threads [NT/2, NT): sweep 2 of every batch
-    // once its factor is published, and the column partials. Each warp waits on
-    // one barrier per batch and keeps twice the independent work per wait.
+    // slice (chunks t + k*NT/2, k < 2V; factors in TMEM for V >= 3, else in
+    // registers), the row partials and a per-row exact-path mask per warp.
+    // Threads [NT/2, NT): sweep 2 of every batch once its factors are published,
+    // and the column partials. Each warp waits on one barrier per batch and
+    // keeps twice the independent work per wait.
     constexpr int NT2 = NT / 2, V2 = 2 * V, NW2 = NW / 2;
     const bool sweep1_role = tid < NT2;
     const unsigned t = sweep1_role ? tid : tid - NT2;
@@ -857,42 +860,59 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
     if (sweep1_role) {
       ScreenBounds sb1;
       const uint32_t tc = tbase + (static_cast<uint32_t>(32 * (w % 4)) << 16) + 8 * V2 * (w / 4);
+      double beta[TB ? 1 : 4 * V2];  // (register factors: V2 <= 4)
       {
-        double beta[4 * V2];
+        double bl[4 * V2];
         const double* bsrc = a.beta2 + ((ctl->iter + 1) & 1ull) * a.pitch + static_cast<size_t>(g) * a.slice;
 #pragma unroll
         for (int k = 0; k < V2; ++k) {
           const unsigned q = t + k * NT2;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) beta[4 * k + e] = (FULL || q < nq) ? bsrc[4 * q + e] : 1.0;
+          for (int e = 0; e < 4; ++e) bl[4 * k + e] = (FULL || q < nq) ? bsrc[4 * q + e] : 1.0;
         }
-        sb1 = screen_bounds(beta, 4 * V2);
+        sb1 = screen_bounds(bl, 4 * V2);
+        if constexpr (TB) {
 #pragma unroll
-        for (int k = 0; k < V2; ++k) tmem_st_chunk(tc + 8 * k, beta + 4 * k);
-        tmem_wait_st_();
+          for (int k = 0; k < V2; ++k) tmem_st_chunk(tc + 8 * k, bl + 4 * k);
+          tmem_wait_st_();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4 * V2; ++i) beta[i] = bl[i];
+        }
       }
       for (unsigned s = 0;; ++s) {
         const unsigned slot = s % NBUF;
         mbar_wait(&full[slot], (s / NBUF) & 1u);
         if (srow[slot] == kNoRow) break;
-        bool bad = false;
-        const double part = row_sweep1_tb<NT2, V2, FULL>(
-            reinterpret_cast<float4*>(smem + slot * a.buf_stride), t, nq, tc, sb1, bad);
-        const double ts = warp_sum(part);
-        const unsigned any_bad = __any_sync(0xffffffffu, bad);
+        const unsigned nr = BM == 1 ? 1u : rows_at(srow[slot]);
         const unsigned q = s % QD;
-        if (lane == 0) {
-          red[q * NW2 + w] = ts;
-          xbad[q * NW2 + w] = any_bad;
+        uint32_t badm = 0;
+#pragma unroll
+        for (int r = 0; r < BM; ++r) {
+          if (r < static_cast<int>(nr)) {
+            bool bad = false;
+            float4* rowp = reinterpret_cast<float4*>(smem + slot * a.buf_stride) + r * (a.slice / 4);
+            double part;
+            if constexpr (TB)
+              part = row_sweep1_tb<NT2, V2, FULL>(rowp, t, nq, tc, sb1, bad);
+            else
+              part = row_sweep1<NT2, V2, FULL>(rowp, t, nq, beta, sb1, bad);
+            const double ts = warp_sum(part);
+            if (__any_sync(0xffffffffu, bad)) badm |= 1u << r;
+            if (lane == 0) red[(q * NW2 + w) * BM + r] = ts;
+          }
         }
+        if (lane == 0) xbad[q * NW2 + w] = badm;
         __syncwarp();
         if (lane == 0) mbar_arrive(&done1[q]);
       }
-      tmem_fence_before_();
-      asm volatile("bar.sync 1, %0;" ::"n"(NT2) : "memory");
-      if (w == 0) {
-        tmem_fence_after_();
-        tmem_dealloc_cols<kTbCols>(tbase);
+      if constexpr (TB) {
+        tmem_fence_before_();
+        asm volatile("bar.sync 1, %0;" ::"n"(NT2) : "memory");
+        if (w == 0) {
+          tmem_fence_after_();
+          tmem_dealloc_cols<kTbCols>(tbase);
+        }
       }
     } else {
       double acc2[4 * V2];
@@ -902,8 +922,13 @@ __global__ void __launch_bounds__(NT + 32 * (1 + NF), 1) sweep_kernel(const Swee
         const unsigned q = b % QD, slot = b % NBUF;
         mbar_wait(&alpha_rdy[q], (b / QD) & 1u);
         if (srow[slot] == kNoRow) break;  // (the factor warps' sentinel completed this phase)
-        row_sweep2<NT2, V2, FULL>(reinterpret_cast<float4*>(smem + slot * a.buf_stride), t, nq, alpha_s[q],
-                                  xbad[q * NW2 + w] != 0u, acc2);
+        const unsigned nr = BM == 1 ? 1u : rows_at(srow[slot]);
+        const uint32_t badm = xbad[q * NW2 + w];
+#pragma unroll
+        for (int r = 0; r < BM; ++r)
+          if (r < static_cast<int>(nr))
+            row_sweep2<NT2, V2, FULL>(reinterpret_cast<float4*>(smem + slot * a.buf_stride) + r * (a.slice / 4), t,
+                                      nq, alpha_s[q * BM + r], (badm >> r) & 1u, acc2);
         fence_proxy_async_smem();  // generic writes -> the producer's bulk store
         __syncwarp();
         if (lane == 0) mbar_arrive(&done2[slot]);
