@@ -47,8 +47,10 @@ struct SweepCfg {
 
 // Sweep 2 lags sweep 1 by kLag = 2 extra batches (the factor warps' budget: the
 // pow and, for G > 1, the L2 exchange round trip). Factor warps alternate
-// batches: 3 for G == 1, 2 when G > 1 (measured: more warps polling L2 cost
-// more issue slots than they buy).
+// batches: 3 (with split sweep roles the factor chain of a G > 1 group — warp
+// partials, L2 exchange, f64 pow — paces sweep 2: 3 warps measured -1.5% at
+// 32768^2 against 2; 4 warps exceed the register budget. Before the split, 2
+// were faster for G > 1: more warps polling L2 cost more issue slots.)
 // (Measured: a lag of 3 for G > 1 — more slack between a group's CTAs — is
 // 10-15% slower: the 7-slot ring then prefetches only two batches.)
 // L2 bytes (all CTAs together) written evict_last at the end of a streaming sweep
@@ -59,7 +61,7 @@ constexpr uint64_t kKeepL2Bytes = 48ull << 20;
 constexpr int kLag = 2;
 constexpr int kLagX = 2;
 constexpr int kFactorWarpsG1 = 3;
-constexpr int kFactorWarpsX = 2;
+constexpr int kFactorWarpsX = 3;
 // Column factors of sweep 1 parked in TMEM (sweep.cuh, TB) for slices of 3-4
 // float4 per thread: frees the registers that otherwise spill (measured +5-8%
 // at 32768^2 .. 16384^2; at V = 2 the factors fit registers and TMEM loses).

@@ -52,7 +52,7 @@ def test_library_is_sm100a_code(uot):
     assert "sm_100a" in out
 
 
-HEADLINE = "_ZN4uotk12sweep_kernelILi512ELi4ELi1ELi7ELi2ELb1ELi2ELb1ELb0EfLb1EEEvNS_9SweepArgsE"
+HEADLINE = "_ZN4uotk12sweep_kernelILi512ELi4ELi1ELi7ELi2ELb1ELi3ELb1ELb0EfLb1EEEvNS_9SweepArgsE"
 
 
 def headline_sass(so):

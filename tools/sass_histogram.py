@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SO = os.path.join(ROOT, "paper_2412_11079_b200", "libuot_cuda.so")
 LOG = os.path.join(ROOT, "paper_2412_11079_b200", "build.log")
-HEADLINE = "_ZN4uotk12sweep_kernelILi512ELi4ELi1ELi7ELi2ELb1ELi2ELb1ELb0EfLb1EEEvNS_9SweepArgsE"
+HEADLINE = "_ZN4uotk12sweep_kernelILi512ELi4ELi1ELi7ELi2ELb1ELi3ELb1ELb0EfLb1EEEvNS_9SweepArgsE"
 
 name = sys.argv[1] if len(sys.argv) > 1 else HEADLINE
 sass = subprocess.run(["cuobjdump", "-sass", SO], capture_output=True, text=True, check=True).stdout
