@@ -142,6 +142,25 @@ def test_alternating_sweeps_keep_rows_in_l2(gpu, orc, m, n, dt):
                 assert np.array_equal(x, y)
 
 
+@pytest.mark.parametrize("m,n", [(600, 8192), (200, 32768), (900, 4096), (500, 20000)])
+def test_split_roles_exact_path(gpu, orc, m, n):
+    """The split sweep roles (V >= 2 slices: 8192 columns G = 1, 32768 G = 4, 4096
+    columns in 2-row batches, 20000 partial slices G = 3) on inputs that fail the
+    fast-path screen — subnormal, zero-adjacent and huge entries — and on rows whose
+    factor leaves the certified range: the sweep-1 warps' exact-path masks reach
+    their sweep-2 partners and the plan stays bit-identical to the oracle."""
+    a, rpd, cpd = orc.gen_problem(91, m, n)
+    a[3, 5] = np.float32(1e-40)                     # subnormal input
+    a[7, n - 1] = np.float32(2e-38)                 # product underflows after scaling
+    a[m // 2, n // 3] = np.float32(3e37)            # product overflows the screen window
+    a[m - 2, :] *= np.float32(1e-30)                # a row whose factor leaves [2^-20, 2^20]
+    ref = orc.fused_solve(a, rpd, cpd, 1.0, 0.1, KNEVER, 4, 4)
+    p, f, cs, done, err, conv, lay = run(gpu, a, rpd, cpd, 1.0, 0.1, 4, resident=False)
+    assert lay["resident"] == 0 and done == 4
+    assert np.array_equal(p, ref.plan), f"{m}x{n}: max rel {np.max(np.abs(p.astype(np.float64) - ref.plan) / ref.plan):.3e}"
+    np.testing.assert_allclose(f.alpha, ref.alpha, rtol=1e-12)
+
+
 @pytest.mark.slow
 def test_default_schedule_is_bit_reproducible_at_scale(gpu):
     """Two default runs (separate sessions) of problems far past the 64 MiB
